@@ -1,0 +1,279 @@
+"""ctypes binding of libmlmq.so (include/mlmq.h).
+
+The product path has no CPU fallback: if the library or a CUDA device is missing,
+solves raise ``EngineError``.  Status codes map onto the reference's exception
+types: EINVAL -> ValueError, EOVERFLOW -> QueueOverflowError,
+everything else -> EngineError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import Optional
+
+import numpy as np
+
+from .core import EngineError, QueueOverflowError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmlmq.so")
+
+MLMQ_OK, MLMQ_EINVAL, MLMQ_EOVERFLOW, MLMQ_EENGINE, MLMQ_ECUDA, MLMQ_ENOMEM = range(6)
+W_U32, W_F32, W_UNIT = 0, 1, 2
+DIST_AUTO, DIST_U32, DIST_U64 = 0, 1, 2
+GEN_KINDS = {"grid2d": 0, "path": 1, "uniform": 2, "rmat": 3}
+GROUP_METRIC_FIELDS = 11
+
+
+class Config(ctypes.Structure):
+    """mlmq_config_t"""
+    _fields_ = [
+        ("l1_type", ctypes.c_int32), ("l2_type", ctypes.c_int32),
+        ("l0_capacity", ctypes.c_int32), ("l1_capacity", ctypes.c_int32),
+        ("wb", ctypes.c_int32),
+        ("delta_nf", ctypes.c_double), ("filter_f", ctypes.c_double), ("delta", ctypes.c_double),
+        ("block_size", ctypes.c_int32), ("block_num", ctypes.c_int64),
+        ("bmax", ctypes.c_int32), ("bnum", ctypes.c_int32),
+        ("node_batch", ctypes.c_int32), ("pnum", ctypes.c_int32),
+        ("num_groups", ctypes.c_int32), ("lanes_per_group", ctypes.c_int32),
+        ("th_v", ctypes.c_int32), ("dup_elim", ctypes.c_int32),
+        ("unit_weights", ctypes.c_int32), ("dist_mode", ctypes.c_int32),
+        ("watchdog_s", ctypes.c_double), ("spin_timeout_s", ctypes.c_double),
+        ("hub_chunk", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7),
+    ]
+
+
+class Metrics(ctypes.Structure):
+    """mlmq_metrics_t"""
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "relaxations", "distance_updates", "l0_enqueues", "l0_dequeues", "l1_enqueues",
+        "l1_dequeues", "l2_enqueues", "l2_dequeues", "l2_atomic_ops", "flushes",
+        "settled_reads", "wall_time_us")] + [
+        ("kernel_ms", ctypes.c_double), ("num_groups", ctypes.c_uint64),
+        ("hub_items", ctypes.c_uint64), ("dist_bits", ctypes.c_uint32),
+        ("reruns", ctypes.c_uint32)]
+
+
+class GenParams(ctypes.Structure):
+    """mlmq_gen_params_t"""
+    _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("m", ctypes.c_int64), ("scale", ctypes.c_int64), ("edge_factor", ctypes.c_int64),
+                ("a", ctypes.c_double), ("b", ctypes.c_double), ("c", ctypes.c_double),
+                ("d", ctypes.c_double), ("wmin", ctypes.c_int64), ("wmax", ctypes.c_int64)]
+
+
+#: every symbol include/mlmq.h declares (checked by tests/test_native_abi.py)
+EXPORTED_SYMBOLS = (
+    "mlmq_abi_version", "mlmq_last_error", "mlmq_device_count", "mlmq_device_info",
+    "mlmq_graph_create", "mlmq_graph_destroy", "mlmq_graph_device_bytes", "mlmq_auto_groups",
+    "mlmq_sssp", "mlmq_sssp_f32", "mlmq_sssp_device", "mlmq_last_dist", "mlmq_reach",
+    "mlmq_feature_sums", "mlmq_gen_size", "mlmq_gen_graph", "mlmq_build_csr",
+    "mlmq_gen_f32_weights",
+)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib():
+    """Load libmlmq.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise EngineError(
+                f"{LIB_PATH} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                " or `make -C paper_2602_10080_b200/csrc`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, U64, I32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int
+        sig = {
+            "mlmq_abi_version": ([], I32),
+            "mlmq_last_error": ([], ctypes.c_char_p),
+            "mlmq_device_count": ([P], I32),
+            "mlmq_device_info": ([I32, P, P, P], I32),
+            "mlmq_graph_create": ([P, P, P, I32, U64, U64, I32, P], I32),
+            "mlmq_graph_destroy": ([P], None),
+            "mlmq_graph_device_bytes": ([P, P], I32),
+            "mlmq_auto_groups": ([P, P, P], I32),
+            "mlmq_sssp": ([P, U64, P, P, P, P, U64], I32),
+            "mlmq_sssp_f32": ([P, U64, P, P, P, P, U64], I32),
+            "mlmq_sssp_device": ([P, U64, P, P], I32),
+            "mlmq_last_dist": ([P, P], I32),
+            "mlmq_reach": ([P, P, P], I32),
+            "mlmq_feature_sums": ([P, P], I32),
+            "mlmq_gen_size": ([I32, P, P, P], I32),
+            "mlmq_gen_graph": ([I32, P, P, U64, P, P, P], I32),
+            "mlmq_build_csr": ([U64, U64, P, P, P, P, P, P, P], I32),
+            "mlmq_gen_f32_weights": ([U64, U64, P], I32),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        if L.mlmq_abi_version() != 1:
+            raise EngineError("libmlmq.so ABI version mismatch")
+        _lib = L
+        return L
+
+
+def last_error() -> str:
+    msg = lib().mlmq_last_error()
+    return msg.decode("utf-8", "replace") if msg else ""
+
+
+def check(status: int) -> None:
+    if status == MLMQ_OK:
+        return
+    msg = last_error()
+    if status == MLMQ_EINVAL:
+        raise ValueError(msg)
+    if status == MLMQ_EOVERFLOW:
+        raise QueueOverflowError(msg)
+    raise EngineError(msg or f"libmlmq error {status}")
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    lib().mlmq_device_count(ctypes.byref(n))
+    return int(n.value)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+class DeviceGraph:
+    """A CSR graph resident in device memory (owns an ``mlmq_graph*``)."""
+
+    def __init__(self, row_offsets: np.ndarray, col: np.ndarray, weights: Optional[np.ndarray],
+                 weight_kind: int, device: int = 0):
+        L = lib()
+        if device_count() < 1:
+            raise EngineError("no CUDA device is visible; the MLMQ engine has no CPU fallback")
+        self._lib = L
+        self.row_offsets = np.ascontiguousarray(row_offsets, dtype=np.uint64)
+        self.col = np.ascontiguousarray(col, dtype=np.uint32)
+        self.n = int(self.row_offsets.size - 1)
+        self.m = int(self.col.size)
+        self.weight_kind = weight_kind
+        w = None
+        if weight_kind == W_U32:
+            w = np.ascontiguousarray(weights, dtype=np.uint32)
+        elif weight_kind == W_F32:
+            w = np.ascontiguousarray(weights, dtype=np.float32)
+        h = ctypes.c_void_p()
+        check(L.mlmq_graph_create(_ptr(self.row_offsets), _ptr(self.col), _ptr(w), weight_kind,
+                                  self.n, self.m, device, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.mlmq_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def auto_groups(self, cfg: Config) -> int:
+        out = ctypes.c_int32(0)
+        check(self._lib.mlmq_auto_groups(self.handle, ctypes.byref(cfg), ctypes.byref(out)))
+        return int(out.value)
+
+    def sssp(self, source: int, cfg: Config, want_groups: int = 0):
+        """Run one solve; returns (dist ndarray, Metrics, group metrics ndarray)."""
+        m = Metrics()
+        gm = np.zeros((max(want_groups, 1), GROUP_METRIC_FIELDS), dtype=np.uint64)
+        if self.weight_kind == W_F32:
+            dist = np.empty(self.n, dtype=np.float32)
+            st = self._lib.mlmq_sssp_f32(self.handle, source, ctypes.byref(cfg), _ptr(dist),
+                                         ctypes.byref(m), _ptr(gm), want_groups)
+        else:
+            dist = np.empty(self.n, dtype=np.uint64)
+            st = self._lib.mlmq_sssp(self.handle, source, ctypes.byref(cfg), _ptr(dist),
+                                     ctypes.byref(m), _ptr(gm), want_groups)
+        check(st)
+        return dist, m, gm
+
+    def sssp_device(self, source: int, cfg: Config) -> Metrics:
+        """Solve leaving distances on the device (benchmark path)."""
+        m = Metrics()
+        check(self._lib.mlmq_sssp_device(self.handle, source, ctypes.byref(cfg), ctypes.byref(m)))
+        return m
+
+    def last_dist(self) -> np.ndarray:
+        dt = np.float32 if self.weight_kind == W_F32 else np.uint64
+        out = np.empty(self.n, dtype=dt)
+        check(self._lib.mlmq_last_dist(self.handle, _ptr(out)))
+        return out
+
+    def reach(self):
+        v, e = ctypes.c_uint64(), ctypes.c_uint64()
+        check(self._lib.mlmq_reach(self.handle, ctypes.byref(v), ctypes.byref(e)))
+        return int(v.value), int(e.value)
+
+    def feature_sums(self) -> np.ndarray:
+        out = np.zeros(10, dtype=np.uint64)
+        check(self._lib.mlmq_feature_sums(self.handle, _ptr(out)))
+        return out
+
+    def device_bytes(self) -> int:
+        out = ctypes.c_uint64()
+        check(self._lib.mlmq_graph_device_bytes(self.handle, ctypes.byref(out)))
+        return int(out.value)
+
+
+def seed_key(seed: int) -> np.ndarray:
+    """CPython random_seed key: 32-bit little-endian limbs of |seed| ({0} for 0)."""
+    s = abs(int(seed))
+    limbs = []
+    while s:
+        limbs.append(s & 0xFFFFFFFF)
+        s >>= 32
+    return np.asarray(limbs or [0], dtype=np.uint32)
+
+
+def generate(kind: str, seed: int, params: dict):
+    """Native generator: returns (row_offsets u64, col u32, weights u32)."""
+    L = lib()
+    gp = GenParams()
+    for k, v in params.items():
+        setattr(gp, k, v)
+    n, m = ctypes.c_uint64(), ctypes.c_uint64()
+    check(L.mlmq_gen_size(GEN_KINDS[kind], ctypes.byref(gp), ctypes.byref(n), ctypes.byref(m)))
+    off = np.empty(n.value + 1, dtype=np.uint64)
+    col = np.empty(m.value, dtype=np.uint32)
+    w = np.empty(m.value, dtype=np.uint32)
+    key = seed_key(seed)
+    check(L.mlmq_gen_graph(GEN_KINDS[kind], ctypes.byref(gp), _ptr(key), key.size,
+                           _ptr(off), _ptr(col), _ptr(w)))
+    return off, col, w
+
+
+def build_csr_native(n: int, src: np.ndarray, dst: np.ndarray, w: np.ndarray):
+    L = lib()
+    src = np.ascontiguousarray(src, dtype=np.uint32)
+    dst = np.ascontiguousarray(dst, dtype=np.uint32)
+    w = np.ascontiguousarray(w, dtype=np.uint32)
+    m = src.size
+    off = np.empty(n + 1, dtype=np.uint64)
+    col = np.empty(m, dtype=np.uint32)
+    wo = np.empty(m, dtype=np.uint32)
+    kept = ctypes.c_uint64()
+    check(L.mlmq_build_csr(n, m, _ptr(src), _ptr(dst), _ptr(w), _ptr(off), _ptr(col), _ptr(wo),
+                           ctypes.byref(kept)))
+    k = int(kept.value)
+    return off, col[:k].copy(), wo[:k].copy()
+
+
+def f32_weights(m: int, seed: int) -> np.ndarray:
+    out = np.empty(m, dtype=np.float32)
+    check(lib().mlmq_gen_f32_weights(m, seed, _ptr(out)))
+    return out

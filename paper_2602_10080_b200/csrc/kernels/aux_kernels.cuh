@@ -1,0 +1,209 @@
+// aux_kernels.cuh — K3 init/bootstrap, ring reset, K5 audit, K4 features, reach, widen.
+#pragma once
+#include "common.cuh"
+
+namespace mlmq {
+
+// Full reset of every queue structure (first use of a workspace, or after an aborted
+// solve left tickets dangling).  Vyukov slots start with seq[s] = s.
+__global__ void reset_queues_kernel(unsigned long long* seq, unsigned long long nslots_total,
+                                    unsigned long long bn_mask, unsigned long long* ptrs,
+                                    int nrings, unsigned long long* hub_seq,
+                                    unsigned long long hub_cap, unsigned long long* ctl,
+                                    uint32_t* hlock, unsigned long long* hsize,
+                                    unsigned long long* hwc, int nheaps) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < nslots_total; i += stride) seq[i] = i & bn_mask;
+  for (unsigned long long i = tid; i < hub_cap; i += stride) hub_seq[i] = i;
+  for (unsigned long long i = tid; i < (unsigned long long)nrings * 32; i += stride) ptrs[i] = 0;
+  for (unsigned long long i = tid; i < (unsigned long long)nheaps; i += stride) {
+    hlock[i * 32] = 0;
+    hsize[i * 16] = 0;
+    hwc[i * 16] = 0;
+  }
+  if (tid == 0) {
+    ctl[C_HUB_WP] = 0;
+    ctl[C_HUB_RP] = 0;
+  }
+}
+
+// K3 (DistanceTable.__init__ core.py:198-203 + mlmq_bootstrap compose.py:92-101):
+// dist = INF except dist[s] = 0; control words reset; done := current reserve total;
+// (s, 0) written straight through to the L2 queue.
+template <class S>
+__global__ void init_kernel(S* dist, unsigned long long n, unsigned long long source, S inf,
+                            KParams p, int l2k) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n; i += stride) dist[i] = (i == source) ? (S)0 : inf;
+  if (tid != 0) return;
+  unsigned long long* ctl = p.ctl;
+  ctl[C_STOP] = 0;
+  ctl[C_ERR] = 0;
+  ctl[C_EPOCH] = 0;
+  ctl[C_DIST_OVF] = 0;
+  ctl[C_LOCAL_NONEMPTY] = 0;
+  ctl[C_HUB_ITEMS] = 0;
+  for (int i = 0; i < 4; ++i) ctl[C_DIAG + i] = 0;
+  unsigned long long reserve = ctl[C_HUB_WP];
+  for (int r = 0; r < p.nrings; ++r) reserve += p.ptrs[(size_t)r * 32];
+  for (int h = 0; h < p.pnum; ++h) reserve += p.hwc[(size_t)h * 16];
+  ctl[C_DONE] = reserve;
+  if (l2k == L2K_HEAP) {
+    Elem<S> e;
+    e.v = (uint32_t)source;
+    e.d = 0;
+    reinterpret_cast<Elem<S>*>(p.hnodes)[0] = e;
+    p.hcnt[0] = 1;
+    p.hsize[0] = 1;
+    p.hwc[0] += 1;
+  } else {
+    const unsigned long long t = p.ptrs[0];
+    const unsigned long long slot = t & p.bn_mask;
+    if (p.seq[slot] != t) ctl[C_ERR] = 99;  // inconsistent ring: host resets and retries
+    Elem<S> e;
+    e.v = (uint32_t)source;
+    e.d = 0;
+    reinterpret_cast<Elem<S>*>(p.data)[slot * p.bs] = e;
+    p.cnt[slot] = 1;
+    p.seq[slot] = t + 1;
+    p.ptrs[0] = t + 1;
+  }
+  __threadfence();
+}
+
+// K5 (_Run.audit engine.py:229-242): reserve == done, rings drained, heaps empty,
+// no group holding elements.
+__global__ void audit_kernel(KParams p, unsigned long long* out) {
+  __shared__ unsigned long long s_res[256], s_bad[256], s_hs[256];
+  const int t = threadIdx.x;
+  unsigned long long res = 0, bad = 0, hs = 0;
+  for (int r = t; r < p.nrings; r += blockDim.x) {
+    const unsigned long long w = p.ptrs[(size_t)r * 32], rd = p.ptrs[(size_t)r * 32 + 16];
+    res += w;
+    bad += (w != rd);
+  }
+  for (int h = t; h < p.pnum; h += blockDim.x) {
+    res += p.hwc[(size_t)h * 16];
+    hs += p.hsize[(size_t)h * 16];
+  }
+  s_res[t] = res;
+  s_bad[t] = bad;
+  s_hs[t] = hs;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (t < o) {
+      s_res[t] += s_res[t + o];
+      s_bad[t] += s_bad[t + o];
+      s_hs[t] += s_hs[t + o];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    const unsigned long long* ctl = p.ctl;
+    out[0] = ctl[C_DONE];
+    out[1] = s_res[0] + ctl[C_HUB_WP];
+    out[2] = s_bad[0];
+    out[3] = ctl[C_HUB_WP] != ctl[C_HUB_RP];
+    out[4] = s_hs[0];
+    out[5] = ctl[C_LOCAL_NONEMPTY];
+    out[6] = ctl[C_ERR];
+    out[7] = ctl[C_DIST_OVF];
+    for (int i = 0; i < 4; ++i) out[8 + i] = ctl[C_DIAG + i];
+    out[12] = ctl[C_HUB_ITEMS];
+    out[13] = ctl[C_EPOCH];
+  }
+}
+
+// u32 device distances -> u64 API distances (INF -> 2^64-1).
+__global__ void widen_kernel(const uint32_t* in, unsigned long long* out, unsigned long long n) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n; i += stride) {
+    const uint32_t v = in[i];
+    out[i] = v == 0xFFFFFFFFu ? ~0ull : (unsigned long long)v;
+  }
+}
+
+// V_reach / E_reach of the device distances.
+template <class S>
+__global__ void reach_kernel(const S* dist, S inf, const unsigned long long* off,
+                             unsigned long long n, unsigned long long* out) {
+  unsigned long long v = 0, e = 0;
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n; i += stride)
+    if (dist[i] != inf) {
+      ++v;
+      e += off[i + 1] - off[i];
+    }
+  v = warp_sum_u64(v);
+  e = warp_sum_u64(e);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, v);
+    atomicAdd(out + 1, e);
+  }
+}
+
+// 128-bit accumulate (lo, hi) for exact sums of squares
+__device__ __forceinline__ void add128(unsigned long long* lo_hi, unsigned long long x) {
+  const unsigned long long old = atomicAdd(lo_hi, x);
+  if (old + x < old) atomicAdd(lo_hi + 1, 1ull);
+}
+
+// K4 (extract_features graph.py:428-460) as exact integer sums:
+// out: [0] sum deg, [1..2] sum deg^2 (lo, hi), [3] max deg,
+//      [4] sum w, [5..6] sum w^2 (lo, hi), [7] max w     (integer weights)
+__global__ void feature_sums_kernel(const unsigned long long* off, const uint2* adj,
+                                    unsigned long long n, unsigned long long m, int unit,
+                                    unsigned long long* out) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long sd = 0, sd2 = 0, sd2_hi = 0, md = 0, sw = 0, sw2 = 0, sw2_hi = 0, mw = 0;
+  for (unsigned long long i = tid; i < n; i += stride) {
+    const unsigned long long d = off[i + 1] - off[i];
+    sd += d;
+    const unsigned long long before = sd2;
+    sd2 += d * d;
+    sd2_hi += sd2 < before;
+    md = d > md ? d : md;
+  }
+  for (unsigned long long k = tid; k < m; k += stride) {
+    const unsigned long long w = unit ? 1ull : (unsigned long long)adj[k].y;
+    sw += w;
+    const unsigned long long before = sw2;
+    sw2 += w * w;
+    sw2_hi += sw2 < before;
+    mw = w > mw ? w : mw;
+  }
+  atomicAdd(out + 0, sd);
+  add128(out + 1, sd2);
+  if (sd2_hi) atomicAdd(out + 2, sd2_hi);
+  atomicMax(out + 3, md);
+  atomicAdd(out + 4, sw);
+  add128(out + 5, sw2);
+  if (sw2_hi) atomicAdd(out + 6, sw2_hi);
+  atomicMax(out + 7, mw);
+}
+
+// float-weight features: out[0] = sum w, out[1] = sum w^2 (double), maxbits = max w bits
+__global__ void feature_sums_f32_kernel(const uint2* adj, unsigned long long m, double* out,
+                                        unsigned int* maxbits) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  double sw = 0, sw2 = 0;
+  unsigned int mw = 0;
+  for (unsigned long long k = tid; k < m; k += stride) {
+    const unsigned int b = adj[k].y;
+    const double w = (double)__uint_as_float(b);
+    sw += w;
+    sw2 += w * w;
+    mw = b > mw ? b : mw;
+  }
+  atomicAdd(out + 0, sw);
+  atomicAdd(out + 1, sw2);
+  atomicMax(maxbits, mw);
+}
+
+}  // namespace mlmq

@@ -1,0 +1,250 @@
+// common.cuh — shared device vocabulary of the MLMQ engine (sm_100a).
+//
+// Distance kinds, queue elements, memory-ordering helpers and the kernel parameter
+// block.  Reference vocabulary: core.py:14-32 (Element, INF, defaults).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mlmq {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+// Device distance kinds.  The API domain is u64 with INF = 2^64-1 (core.py:17-18);
+// the engine runs u32 when the result provably (or, optimistically, actually) fits,
+// and f32 for float-weight graphs.
+enum { DK_U32 = 0, DK_U64 = 1, DK_F32 = 2 };
+// L2 kernel families: FIFO ring, bucket (Δ window over rings), batch heap
+// (priority = one heap, multi = pnum heaps).
+enum { L2K_FIFO = 0, L2K_BUCKET = 1, L2K_HEAP = 2 };
+enum { L1K_VECTOR = 0, L1K_NEAR_FAR = 1, L1K_FILTER = 2, L1K_SLF = 3 };
+
+enum {
+  ERR_NONE = 0,
+  ERR_OVERFLOW = 1,      // ring slot stayed busy (l2.py:116-135)
+  ERR_ABORT = 2,         // host watchdog abort (engine.py:267-272)
+  ERR_HEAP_OVERFLOW = 3, // batch-heap node pool exhausted
+  ERR_HUB_OVERFLOW = 4   // hub work ring slot stayed busy
+};
+
+// Control block: u64 words, every hot word on its own 128-byte line.
+enum : int {
+  C_DONE = 0,             // global_done (l2.py:33-70), in queue units
+  C_STOP = 16,            // work flag cleared by the manager (engine.py:152-169)
+  C_ERR = 32,             // ERR_* code
+  C_EPOCH = 48,           // bucket floor index (l2.py:181-301)
+  C_HUB_WP = 64,          // hub ring write ticket
+  C_HUB_RP = 80,          // hub ring read ticket
+  C_DIST_OVF = 96,        // optimistic u32 distance overflowed
+  C_LOCAL_NONEMPTY = 112, // audit: sum of L0+L1 sizes at exit (engine.py:233-237)
+  C_DIAG = 128,           // overflow diagnostics: ring, slot, write_ptr, read_ptr
+  C_HUB_ITEMS = 144,      // hub items pushed
+  C_WORDS = 160
+};
+
+// Per-group metric slots, in METRIC_FIELDS order (core.py:142-154).
+enum {
+  M_RELAX = 0, M_UPD, M_L0E, M_L0D, M_L1E, M_L1D, M_L2E, M_L2D, M_L2A, M_FLUSH, M_SETTLED,
+  M_COUNT
+};
+
+template <int K> struct DT;
+
+template <> struct DT<DK_U32> {
+  using S = uint32_t;
+  static constexpr uint32_t INF = 0xFFFFFFFFu;
+  __device__ __forceinline__ static S add(S a, uint32_t w, bool& ovf) {
+    uint64_t s = (uint64_t)a + w;
+    if (s >= 0xFFFFFFFFull) { ovf = true; return INF; }
+    return (S)s;
+  }
+  // saturating add for thresholds (NF / F rebases); never produces INF
+  __device__ __forceinline__ static S add_thr(S a, S b) {
+    uint64_t s = (uint64_t)a + b;
+    return s >= 0xFFFFFFFFull ? (S)0xFFFFFFFEu : (S)s;
+  }
+};
+
+template <> struct DT<DK_U64> {
+  using S = unsigned long long;
+  static constexpr unsigned long long INF = ~0ull;
+  __device__ __forceinline__ static S add(S a, uint32_t w, bool& ovf) {
+    S s = a + w;
+    if (s < a || s == INF) { ovf = true; return INF; }
+    return s;
+  }
+  __device__ __forceinline__ static S add_thr(S a, S b) {
+    S s = a + b;
+    return (s < a || s == INF) ? INF - 1 : s;
+  }
+};
+
+// f32 distances live as their IEEE bit patterns; for non-negative floats the unsigned
+// order of the bits is the numeric order, so atomicMin on u32 is a float min.
+template <> struct DT<DK_F32> {
+  using S = uint32_t;
+  static constexpr uint32_t INF = 0x7f800000u;  // +inf
+  __device__ __forceinline__ static S add(S a, uint32_t w, bool&) {
+    return __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(w)));
+  }
+  __device__ __forceinline__ static S add_thr(S a, S b) {
+    return __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(b)));
+  }
+};
+
+// Queue element (core.py:14): (vertex id, tentative distance at enqueue time).
+template <class S> struct Elem;
+template <> struct __align__(8) Elem<uint32_t> {
+  uint32_t v, d;
+};
+template <> struct __align__(16) Elem<unsigned long long> {
+  uint32_t v, pad;
+  unsigned long long d;
+};
+
+// Hub work item: an edge range of one high-degree vertex (new tier).
+struct __align__(16) HubItem {
+  unsigned long long lo, hi;
+  unsigned long long du;  // distance snapshot (S bits)
+  uint32_t u, pad;
+};
+
+// ---------------------------------------------------------------------------------
+// memory-ordering helpers (PTX memory model, gpu scope unless noted)
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// host-mapped pinned word written by the host watchdog
+__device__ __forceinline__ uint32_t ld_sys_u32(const volatile uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// L2-coherent (L1-bypassing) element loads for queue storage that is reused.
+__device__ __forceinline__ Elem<uint32_t> ld_cg_elem(const Elem<uint32_t>* p) {
+  uint2 r = __ldcg(reinterpret_cast<const uint2*>(p));
+  Elem<uint32_t> e;
+  e.v = r.x;
+  e.d = r.y;
+  return e;
+}
+__device__ __forceinline__ Elem<unsigned long long> ld_cg_elem(const Elem<unsigned long long>* p) {
+  uint4 r = __ldcg(reinterpret_cast<const uint4*>(p));
+  Elem<unsigned long long> e;
+  e.v = r.x;
+  e.pad = 0;
+  e.d = ((unsigned long long)r.w << 32) | r.z;
+  return e;
+}
+__device__ __forceinline__ uint32_t ldcg_dist(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned long long ldcg_dist(const unsigned long long* p) { return __ldcg(p); }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// ---------------------------------------------------------------------------------
+// kernel parameter block
+// ---------------------------------------------------------------------------------
+struct KParams {
+  // graph (device CSR; adjacency interleaved as (col, weight bits))
+  const unsigned long long* off;
+  const uint2* adj;
+  unsigned long long n;
+  void* dist;  // S[n]
+  unsigned long long source;
+
+  // resolved config (engine.py:57-103)
+  int L;            // lanes_per_group
+  int l0cap;        // l0_capacity
+  int l1type;       // L1K_*
+  int l1cap;        // l1 capacity
+  int wb;           // flush period
+  int th_v;         // cooperative threshold
+  int dup;          // duplicate elimination
+  int unit;         // unit weights
+  int bs;           // block_size
+  int bmax, bnum;   // bucket window
+  int nb;           // heap node batch (<= 32)
+  int pnum;         // number of heaps (multi)
+  int G;            // worker groups (warps); warp G is the manager
+  unsigned long long delta_nf_s;  // thresholds in distance encoding (S bits)
+  unsigned long long filter_f_s;
+  unsigned long long delta_i;     // bucket Δ, integer kinds
+  double delta_f;                 // bucket Δ, f32 kind
+
+  // L2 rings: nrings rings of bn slots; slot = bs elements
+  unsigned long long* seq;   // [nrings * bn]
+  uint32_t* cnt;             // [nrings * bn]
+  void* data;                // [nrings * bn * bs] elements
+  unsigned long long* ptrs;  // per ring: wp at [r*32], rp at [r*32+16]
+  unsigned long long bn_mask;
+  int nrings;
+
+  // batch heaps
+  uint32_t* hlock;              // [pnum * 32]
+  unsigned long long* hsize;    // [pnum * 16]
+  unsigned long long* hwc;      // [pnum * 16] element write counter (termination units)
+  void* hnodes;                 // [pnum * hcap * 32] elements
+  uint32_t* hcnt;               // [pnum * hcap]
+  unsigned long long hcap;      // nodes per heap
+
+  // hub work ring
+  unsigned long long* hub_seq;
+  HubItem* hub_data;
+  unsigned long long hub_mask;
+  unsigned long long hub_chunk;
+  unsigned long long hub_thresh;
+
+  // control
+  unsigned long long* ctl;
+  const volatile uint32_t* host_abort;
+  unsigned long long* metrics;  // [G * M_COUNT]
+  unsigned long long spin_timeout_ns;
+  int smem_per_warp;            // bytes
+  int batch_cap, out_cap, spill_cap;  // elements
+};
+
+}  // namespace mlmq

@@ -1,0 +1,1256 @@
+// mlmq_kernel.cuh — K1 persistent MLMQ relax kernel + K2 manager warp (sm_100a).
+//
+// One warp = one worker group, one lane = one lane.  Per warp:
+//   L0  per-lane FIFOs of l0_capacity elements held in REGISTERS (l1.py:21-96)
+//   L1  a warp-private shared-memory ring: vector / near_far / filter / slf (l1.py:99-280)
+//   L2  shared HBM queue: ticketed block ring FIFO, Δ-bucket window over rings, or
+//       lock-protected batch heaps (l2.py:73-451)
+// behind the unified Read/Write cascade of compose.py:30-86 (PAPER Listing 1):
+//   Read : L0 -> L1 -> hub items -> L2, served entirely from the first non-empty level;
+//          a full miss flushes local_done into global done (l2.py:56-62).
+//   Write: L0 -> (full transfer) L1 -> (write-back) L2.
+// Relaxation (engine.py:171-227) is warp-cooperative: dup-elim, degree split at th_v,
+// flattened load-balanced expansion of small lists, warp-strided walks of big lists,
+// hub lists split into edge-range work items shared by all warps, atomicMin on dist.
+// Termination is the delayed-count protocol of PAPER.md:589 / l2.py:33-70, counted in
+// queue units (blocks written/read), checked by a manager warp that needs three
+// consecutive equal observations (engine.py:32-33, 152-169).
+#pragma once
+#include "common.cuh"
+
+namespace mlmq {
+
+template <int K, int L2K, int CM>
+struct Worker {
+  using Tr = DT<K>;
+  using S = typename Tr::S;
+  using E = Elem<S>;
+  static constexpr int U = 4;  // edge slots per lane per step
+
+  const KParams& p;
+  S* dist;
+  E* batch;
+  E* outs;
+  E* spill;
+  E* l1a;
+  E* l1b;
+  unsigned long long* met;
+  int lane, gid, L;
+
+  // L0: per-lane register FIFO (shift register, pop at index 0)
+  uint32_t l0v[CM];
+  S l0d[CM];
+  int l0n;
+  int wc, rc, l0size;
+
+  // L1 (ring a: vector/filter/slf/near; ring b: far)
+  int h1, n1, h2, n2;
+  S thr, rej_min;
+  bool has_rej;
+  int wcount;
+
+  unsigned long long local_done;
+  int mcursor;
+  int outn;
+  bool dist_ovf;
+
+  __device__ Worker(const KParams& prm, unsigned char* sm, int g, int ln) : p(prm), lane(ln), gid(g) {
+    L = p.L;
+    dist = reinterpret_cast<S*>(p.dist);
+    E* base = reinterpret_cast<E*>(sm);
+    batch = base;
+    outs = batch + p.batch_cap;
+    spill = outs + p.out_cap;
+    l1a = spill + p.spill_cap;
+    l1b = l1a + p.l1cap;
+    const int l1n = (p.l1type == L1K_NEAR_FAR ? 2 : 1) * p.l1cap;
+    met = reinterpret_cast<unsigned long long*>(l1a + l1n);
+    if (lane < M_COUNT) met[lane] = 0;
+    l0n = 0;
+    wc = rc = l0size = 0;
+    h1 = n1 = h2 = n2 = 0;
+    thr = (S)(p.l1type == L1K_NEAR_FAR ? p.delta_nf_s : p.filter_f_s);
+    rej_min = (S)Tr::INF;
+    has_rej = false;
+    wcount = 0;
+    local_done = 0;
+    mcursor = p.pnum > 0 ? gid % p.pnum : 0;
+    outn = 0;
+    dist_ovf = false;
+    __syncwarp();
+  }
+
+  __device__ __forceinline__ void count(int f, unsigned long long v) {
+    if (lane == 0) met[f] += v;
+  }
+  __device__ __forceinline__ bool stopped() const {
+    return ld_relaxed(p.ctl + C_STOP) != 0;
+  }
+  __device__ __forceinline__ unsigned long long* wp(int r) const { return p.ptrs + (size_t)r * 32; }
+  __device__ __forceinline__ unsigned long long* rp(int r) const { return p.ptrs + (size_t)r * 32 + 16; }
+
+  // Raise a queue error (QueueOverflowError analogue) and stop every warp.
+  __device__ void raise_error(int code, unsigned long long a, unsigned long long b,
+                              unsigned long long c, unsigned long long d) {
+    if (atomicCAS(p.ctl + C_ERR, 0ull, (unsigned long long)code) == 0ull) {
+      p.ctl[C_DIAG + 0] = a;
+      p.ctl[C_DIAG + 1] = b;
+      p.ctl[C_DIAG + 2] = c;
+      p.ctl[C_DIAG + 3] = d;
+    }
+    __threadfence();
+    st_release(p.ctl + C_STOP, 1ull);
+  }
+
+  // ============================================================ L0 (registers)
+  __device__ __forceinline__ void l0_push(uint32_t v, S d) {
+#pragma unroll
+    for (int j = 0; j < CM; ++j)
+      if (j == l0n) { l0v[j] = v; l0d[j] = d; }
+    ++l0n;
+  }
+  __device__ __forceinline__ void l0_pop(uint32_t& v, S& d) {
+    v = l0v[0];
+    d = l0d[0];
+#pragma unroll
+    for (int j = 0; j + 1 < CM; ++j) { l0v[j] = l0v[j + 1]; l0d[j] = l0d[j + 1]; }
+    --l0n;
+  }
+
+  // Drain every lane, lanes in round-robin order from the read cursor, each lane FIFO
+  // (l1.py:87-96).  Returns the number of elements written to dst.
+  __device__ int l0_drain(E* dst) {
+    const int q = lane;
+    const int srcl = (rc + q) % L;
+    int c = __shfl_sync(FULL, l0n, srcl);
+    if (q >= L) c = 0;
+    int incl = warp_incl_scan(c, lane);
+    const int total = __shfl_sync(FULL, incl, 31);
+    const int excl_q = incl - c;
+    const int r = (lane - rc + L) % L;
+    const int ex = __shfl_sync(FULL, excl_q, r & 31);
+    if (lane < L) {
+#pragma unroll
+      for (int j = 0; j < CM; ++j)
+        if (j < l0n) {
+          E e;
+          e.v = l0v[j];
+          e.d = l0d[j];
+          dst[ex + j] = e;
+        }
+      l0n = 0;
+    }
+    __syncwarp();
+    return total;
+  }
+
+  // Pop up to `want`, one per non-empty lane per round from the read cursor
+  // (l1.py:66-85); the cursor ends after the lane that gave the last element.
+  __device__ int l0_read(E* dst, int want) {
+    const int T = min(want, l0size);
+    int taken = 0, last = 0;
+    const unsigned lmask = (L == 32) ? FULL : ((1u << L) - 1u);
+    const int r = (lane - rc + L) % L;
+    while (taken < T) {
+      const bool ne = lane < L && l0n > 0;
+      const unsigned m = __ballot_sync(FULL, ne);
+      const unsigned rot = rc == 0 ? m : (((m >> rc) | (m << (L - rc))) & lmask);
+      const int rank = __popc(rot & ((1u << r) - 1u));
+      const int a = __popc(m);
+      const int t = min(a, T - taken);
+      const bool take = ne && rank < t;
+      if (take) {
+        uint32_t v;
+        S d;
+        l0_pop(v, d);
+        E e;
+        e.v = v;
+        e.d = d;
+        dst[taken + rank] = e;
+      }
+      const unsigned tm = __ballot_sync(FULL, take && rank == t - 1);
+      last = __ffs(tm) - 1;
+      taken += t;
+    }
+    rc = (last + 1) % L;
+    l0size -= T;
+    __syncwarp();
+    return T;
+  }
+
+  // ============================================================ L2: block rings
+  __device__ bool wait_seq(int rid, unsigned long long slot, unsigned long long want) {
+    int ok = 1;
+    if (lane == 0) {
+      unsigned long long* s = p.seq + (size_t)rid * (p.bn_mask + 1) + slot;
+      unsigned long long t0 = 0;
+      int spins = 0, ns = 32;
+      while (ld_acquire(s) != want) {
+        if (++spins % 64 == 0) {
+          if (stopped()) { ok = 0; break; }
+          unsigned long long now = globaltimer_ns();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > p.spin_timeout_ns) {
+            raise_error(ERR_OVERFLOW, (unsigned long long)rid, slot, ld_relaxed(wp(rid)), ld_relaxed(rp(rid)));
+            ok = 0;
+            break;
+          }
+        }
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+      }
+    }
+    return __shfl_sync(FULL, ok, 0) != 0;
+  }
+
+  __device__ __forceinline__ E* slot_data(int rid, unsigned long long slot) const {
+    return reinterpret_cast<E*>(p.data) + ((size_t)rid * (p.bn_mask + 1) + slot) * p.bs;
+  }
+
+  __device__ __forceinline__ void publish(int rid, unsigned long long slot, unsigned long long tk, int c) {
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
+      p.cnt[i] = (uint32_t)c;
+      st_release(p.seq + i, tk + 1);
+    }
+  }
+
+  // Writer (l2.py:96-114): one fetch-add claims ceil(n/bs) tickets, each segment waits
+  // for its slot's sequence number (ABA-safe, unlike bare tags) and is published whole.
+  __device__ void ring_write(int rid, const E* base, int start, int n, int cap) {
+    if (n <= 0) return;
+    const int bs = p.bs;
+    const unsigned long long nseg = (unsigned long long)((n + bs - 1) / bs);
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(wp(rid), nseg);
+    t = __shfl_sync(FULL, t, 0);
+    count(M_L2A, 1);
+    for (unsigned long long s = 0; s < nseg; ++s) {
+      const unsigned long long tk = t + s, slot = tk & p.bn_mask;
+      if (!wait_seq(rid, slot, tk)) return;
+      const int c = min(bs, n - (int)s * bs);
+      E* d = slot_data(rid, slot);
+      for (int i = lane; i < c; i += 32) d[i] = base[(start + (int)s * bs + i) % cap];
+      publish(rid, slot, tk, c);
+    }
+  }
+
+  // Same, with the elements held one per lane (grp = writing lanes, rank within grp).
+  __device__ void ring_write_lanes(int rid, unsigned grp, int rank, const E& x, bool mine) {
+    const int c = __popc(grp);
+    const int bs = p.bs;
+    const unsigned long long nseg = (unsigned long long)((c + bs - 1) / bs);
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(wp(rid), nseg);
+    t = __shfl_sync(FULL, t, 0);
+    count(M_L2A, 1);
+    for (unsigned long long s = 0; s < nseg; ++s) {
+      const unsigned long long tk = t + s, slot = tk & p.bn_mask;
+      if (!wait_seq(rid, slot, tk)) return;
+      if (mine && rank / bs == (int)s) slot_data(rid, slot)[rank % bs] = x;
+      publish(rid, slot, tk, min(bs, c - (int)s * bs));
+    }
+  }
+
+  // Reader (l2.py:137-162): claim a ticket only when a written block exists, then wait
+  // for the in-flight writer (never leaves a dangling claim), copy, free the slot.
+  __device__ int ring_read(int rid, E* dst) {
+    unsigned long long r = 0;
+    int got = 0;
+    if (lane == 0) {
+      unsigned long long* rpp = rp(rid);
+      unsigned long long* wpp = wp(rid);
+      r = ld_relaxed(rpp);
+      unsigned long long w = ld_relaxed(wpp);
+      while (r < w) {
+        unsigned long long old = atomicCAS(rpp, r, r + 1);
+        if (old == r) { got = 1; break; }
+        r = old;
+        if (r >= w) w = ld_relaxed(wpp);
+      }
+    }
+    got = __shfl_sync(FULL, got, 0);
+    if (!got) return 0;
+    r = __shfl_sync(FULL, r, 0);
+    count(M_L2A, 1);
+    const unsigned long long slot = r & p.bn_mask;
+    if (!wait_seq(rid, slot, r + 1)) return 0;
+    __syncwarp();
+    const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
+    int c = 0;
+    if (lane == 0) c = (int)__ldcg(p.cnt + i);
+    c = __shfl_sync(FULL, c, 0);
+    const E* d = slot_data(rid, slot);
+    for (int k = lane; k < c; k += 32) dst[k] = ld_cg_elem(d + k);
+    __syncwarp();
+    if (lane == 0) st_release(p.seq + i, r + p.bn_mask + 1);
+    return c;
+  }
+
+  // ============================================================ L2: bucket window
+  __device__ __forceinline__ int bucket_rel(S d, unsigned long long e) const {
+    if (K == DK_F32) {
+      const double base = (double)e * p.delta_f;
+      const double dv = (double)__uint_as_float((uint32_t)d);
+      if (dv < base) return 0;
+      const double q = floor((dv - base) / p.delta_f);
+      return q >= (double)(p.bmax - 1) ? p.bmax - 1 : (int)q;
+    } else {
+      const unsigned long long base = e * p.delta_i;
+      const unsigned long long dd = (unsigned long long)d;
+      if (dd < base) return 0;
+      const unsigned long long q = (dd - base) / p.delta_i;
+      return q >= (unsigned long long)(p.bmax - 1) ? p.bmax - 1 : (int)q;
+    }
+  }
+
+  // Group the lanes' elements by target bucket ring and write each group as blocks.
+  __device__ void bucket_scatter_lanes(bool has, const E& x, int f) {
+    unsigned act = __ballot_sync(FULL, has);
+    while (act) {
+      const int leader = __ffs(act) - 1;
+      const int fl = __shfl_sync(FULL, f, leader);
+      const bool mine = has && f == fl;
+      const unsigned grp = __ballot_sync(FULL, mine);
+      const int rank = __popc(grp & lanemask_lt());
+      ring_write_lanes(fl, grp, rank, x, mine);
+      act &= ~grp;
+    }
+  }
+
+  // l2.py:209-233: rel = 0 below the floor, (d-base)//Δ above, clamped to bmax-1.
+  __device__ void bucket_write(const E* base, int start, int n, int cap) {
+    const unsigned long long e = ld_relaxed(p.ctl + C_EPOCH);
+    for (int o = 0; o < n; o += 32) {
+      const bool has = o + lane < n;
+      E x;
+      int f = 0;
+      if (has) {
+        x = base[(start + o + lane) % cap];
+        f = (int)((e + (unsigned long long)bucket_rel(x.d, e)) % (unsigned long long)p.bmax);
+      }
+      bucket_scatter_lanes(has, x, f);
+    }
+  }
+
+  // l2.py:235-295: scan bnum buckets from the floor; rebin stale-slot elements; advance
+  // the floor by one when the head is seen empty while elements remain elsewhere.
+  __device__ int bucket_read(E* dst) {
+    const unsigned long long e0 = ld_relaxed(p.ctl + C_EPOCH);
+    bool head_empty = false;
+    for (int j = 0; j < p.bnum; ++j) {
+      const int f = (int)((e0 + (unsigned long long)j) % (unsigned long long)p.bmax);
+      for (;;) {
+        const int c = ring_read(f, dst);
+        if (c == 0) {
+          if (j == 0) head_empty = true;
+          break;
+        }
+        local_done += 1;
+        const unsigned long long en = ld_relaxed(p.ctl + C_EPOCH);
+        const int rel_slot = (int)(((unsigned long long)f + (unsigned long long)p.bmax -
+                                    (en % (unsigned long long)p.bmax)) % (unsigned long long)p.bmax);
+        int kept = 0;
+        for (int o = 0; o < c; o += 32) {
+          const bool has = o + lane < c;
+          E x;
+          int rel = 0;
+          if (has) {
+            x = dst[o + lane];
+            rel = bucket_rel(x.d, en);
+          }
+          __syncwarp();
+          const bool rb = has && rel > rel_slot;
+          const bool keep = has && !rb;
+          const unsigned km = __ballot_sync(FULL, keep);
+          if (keep) dst[kept + __popc(km & lanemask_lt())] = x;
+          kept += __popc(km);
+          if (__any_sync(FULL, rb))
+            bucket_scatter_lanes(rb, x, (int)((en + (unsigned long long)rel) % (unsigned long long)p.bmax));
+          __syncwarp();
+        }
+        if (kept > 0) return kept;
+        if (stopped()) return 0;
+      }
+    }
+    if (head_empty) {
+      bool ne = false;
+      for (int k = lane; k < p.bmax; k += 32)
+        if (k != (int)(e0 % (unsigned long long)p.bmax)) ne |= ld_relaxed(wp(k)) > ld_relaxed(rp(k));
+      if (__any_sync(FULL, ne)) {
+        if (lane == 0 && atomicCAS(p.ctl + C_EPOCH, e0, e0 + 1) == e0) met[M_L2A] += 1;
+        __syncwarp();
+      }
+    }
+    return 0;
+  }
+
+  // ============================================================ L2: batch heaps
+  __device__ __forceinline__ E* node_elems(int h, unsigned long long i) const {
+    return reinterpret_cast<E*>(p.hnodes) + ((size_t)h * p.hcap + i) * 32;
+  }
+  __device__ __forceinline__ uint32_t* node_cnt(int h, unsigned long long i) const {
+    return p.hcnt + (size_t)h * p.hcap + i;
+  }
+  __device__ __forceinline__ S node_min(int h, unsigned long long i) const {
+    S v = 0;
+    if (lane == 0) v = ld_cg_elem(node_elems(h, i)).d;
+    return __shfl_sync(FULL, v, 0);
+  }
+  __device__ void node_swap(int h, unsigned long long a, unsigned long long b) {
+    E* A = node_elems(h, a);
+    E* B = node_elems(h, b);
+    E xa = ld_cg_elem(A + lane), xb = ld_cg_elem(B + lane);
+    uint32_t ca = 0, cb = 0;
+    if (lane == 0) { ca = __ldcg(node_cnt(h, a)); cb = __ldcg(node_cnt(h, b)); }
+    __syncwarp();
+    A[lane] = xb;
+    B[lane] = xa;
+    if (lane == 0) { *node_cnt(h, a) = cb; *node_cnt(h, b) = ca; }
+    __threadfence();
+    __syncwarp();
+  }
+  __device__ bool heap_lock(int h) {
+    int ok = 1;
+    if (lane == 0) {
+      uint32_t* lk = p.hlock + (size_t)h * 32;
+      unsigned long long t0 = 0;
+      int spins = 0, ns = 32;
+      while (atomicCAS(lk, 0u, 1u) != 0u) {
+        if (++spins % 64 == 0) {
+          if (stopped()) { ok = 0; break; }
+          unsigned long long now = globaltimer_ns();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > p.spin_timeout_ns) {
+            raise_error(ERR_OVERFLOW, 1000000ull + h, 0, 0, 0);
+            ok = 0;
+            break;
+          }
+        }
+        __nanosleep(ns);
+        if (ns < 512) ns <<= 1;
+      }
+      __threadfence();
+    }
+    ok = __shfl_sync(FULL, ok, 0);
+    __syncwarp();
+    return ok != 0;
+  }
+  __device__ void heap_unlock(int h) {
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicExch(p.hlock + (size_t)h * 32, 0u);
+  }
+  __device__ void sift_up(int h, unsigned long long i) {
+    while (i > 0) {
+      const unsigned long long par = (i - 1) >> 1;
+      if (node_min(h, i) < node_min(h, par)) {
+        node_swap(h, i, par);
+        i = par;
+      } else
+        break;
+    }
+  }
+  __device__ void sift_down(int h, unsigned long long i, unsigned long long size) {
+    for (;;) {
+      unsigned long long c = 2 * i + 1;
+      if (c >= size) return;
+      if (c + 1 < size && node_min(h, c + 1) < node_min(h, c)) ++c;
+      if (node_min(h, c) < node_min(h, i)) {
+        node_swap(h, i, c);
+        i = c;
+      } else
+        return;
+    }
+  }
+  __device__ __forceinline__ static bool elem_less(S da, uint32_t va, S db, uint32_t vb) {
+    return da < db || (da == db && va < vb);
+  }
+  // bitonic sort of one element per lane (invalid lanes sort last)
+  __device__ void warp_sort(E& x, bool has) {
+    S d = has ? x.d : (S)Tr::INF;
+    uint32_t v = has ? x.v : 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const S pd = __shfl_xor_sync(FULL, d, j);
+        const uint32_t pv = __shfl_xor_sync(FULL, v, j);
+        const bool up = (lane & k) == 0;
+        const bool lower = (lane & j) == 0;
+        const bool take_min = (lower == up);
+        const bool pless = elem_less(pd, pv, d, v);
+        if (pless == take_min) { d = pd; v = pv; }
+      }
+    }
+    x.d = d;
+    x.v = v;
+  }
+  // l2.py:322-344: sorted batch -> nodes of <= node_batch, appended as leaves + sift-up.
+  __device__ void heap_write(int h, const E* base, int start, int n, int cap) {
+    for (int o = 0; o < n; o += 32) {
+      const int c = min(32, n - o);
+      const bool has = lane < c;
+      E x;
+      if (has) x = base[(start + o + lane) % cap];
+      warp_sort(x, has);
+      const int nb = p.nb;
+      const int nn = (c + nb - 1) / nb;
+      if (!heap_lock(h)) return;
+      unsigned long long size = 0;
+      if (lane == 0) size = __ldcg(p.hsize + (size_t)h * 16);
+      size = __shfl_sync(FULL, size, 0);
+      if (size + (unsigned long long)nn > p.hcap) {
+        if (lane == 0) raise_error(ERR_HEAP_OVERFLOW, (unsigned long long)h, size, p.hcap, 0);
+        heap_unlock(h);
+        return;
+      }
+      for (int q = 0; q < nn; ++q) {
+        const unsigned long long i = size + (unsigned long long)q;
+        if (has && lane / nb == q) node_elems(h, i)[lane % nb] = x;
+        if (lane == 0) *node_cnt(h, i) = (uint32_t)min(nb, c - q * nb);
+        // realign so the node's elements start at slot 0 (lanes q*nb .. q*nb+nb-1)
+        __threadfence();
+        __syncwarp();
+        sift_up(h, i);
+      }
+      if (lane == 0) {
+        p.hsize[(size_t)h * 16] = size + (unsigned long long)nn;
+        p.hwc[(size_t)h * 16] += (unsigned long long)c;  // reserve units, before unlock
+      }
+      count(M_L2A, 1);
+      heap_unlock(h);
+    }
+  }
+  // l2.py:362-389: pop runs off the root while root.min <= min(child mins).
+  __device__ int heap_read(int h, E* dst, int want) {
+    if (lane == 0 && ld_relaxed(p.hsize + (size_t)h * 16) == 0) want = -1;
+    if (__shfl_sync(FULL, want, 0) < 0) return 0;
+    if (!heap_lock(h)) return 0;
+    unsigned long long size = 0;
+    if (lane == 0) size = __ldcg(p.hsize + (size_t)h * 16);
+    size = __shfl_sync(FULL, size, 0);
+    int n = 0;
+    while (size > 0 && n < want) {
+      int c0 = 0;
+      if (lane == 0) c0 = (int)__ldcg(node_cnt(h, 0));
+      c0 = __shfl_sync(FULL, c0, 0);
+      E e = ld_cg_elem(node_elems(h, 0) + lane);
+      const bool has_child = size > 1;
+      S cm = (S)Tr::INF;
+      if (has_child) {
+        cm = node_min(h, 1);
+        if (size > 2) {
+          const S c2 = node_min(h, 2);
+          if (c2 < cm) cm = c2;
+        }
+      }
+      const bool take = lane < c0 && (!has_child || e.d <= cm);
+      const int t = min(__popc(__ballot_sync(FULL, take)), want - n);
+      if (lane < t) dst[n + lane] = e;
+      n += t;
+      const int rem = c0 - t;
+      E sh;
+      sh.v = __shfl_sync(FULL, e.v, (lane + t) & 31);
+      sh.d = __shfl_sync(FULL, e.d, (lane + t) & 31);
+      __syncwarp();
+      if (lane < rem) node_elems(h, 0)[lane] = sh;
+      if (lane == 0) *node_cnt(h, 0) = (uint32_t)rem;
+      __threadfence();
+      __syncwarp();
+      const S newmin = __shfl_sync(FULL, sh.d, 0);
+      if (rem == 0) {
+        --size;
+        if (size > 0) {
+          E* R = node_elems(h, 0);
+          E lx = ld_cg_elem(node_elems(h, size) + lane);
+          uint32_t lc = 0;
+          if (lane == 0) lc = __ldcg(node_cnt(h, size));
+          __syncwarp();
+          R[lane] = lx;
+          if (lane == 0) *node_cnt(h, 0) = lc;
+          __threadfence();
+          __syncwarp();
+          sift_down(h, 0, size);
+        }
+      } else if (has_child && newmin > cm) {
+        sift_down(h, 0, size);
+      } else {
+        break;
+      }
+    }
+    if (lane == 0) p.hsize[(size_t)h * 16] = size;
+    if (n > 0) count(M_L2A, 1);
+    heap_unlock(h);
+    local_done += (unsigned long long)n;
+    return n;
+  }
+
+  // ============================================================ L2 dispatch
+  // write_through (compose.py:79-86): the termination reservation is the ring ticket
+  // (or heap write counter) itself, claimed before the block is published.
+  __device__ void write_back(const E* base, int start, int n, int cap) {
+    if (n <= 0) return;
+    count(M_L2E, (unsigned long long)n);
+    if (L2K == L2K_FIFO) {
+      ring_write(0, base, start, n, cap);
+    } else if (L2K == L2K_BUCKET) {
+      bucket_write(base, start, n, cap);
+    } else {
+      heap_write(mcursor, base, start, n, cap);
+      if (p.pnum > 1) mcursor = (mcursor + 1) % p.pnum;
+    }
+  }
+
+  __device__ int l2_read(E* dst) {
+    int c;
+    if (L2K == L2K_FIFO) {
+      c = ring_read(0, dst);
+      if (c > 0) local_done += 1;
+    } else if (L2K == L2K_BUCKET) {
+      c = bucket_read(dst);
+    } else {
+      c = heap_read(p.pnum > 1 ? gid % p.pnum : 0, dst, L);
+    }
+    if (c > 0) count(M_L2D, (unsigned long long)c);
+    return c;
+  }
+
+  // ============================================================ L1 (shared memory)
+  __device__ __forceinline__ static int ridx(int h, int i, int cap) { return (int)(((long long)h + i) % cap); }
+  __device__ __forceinline__ static int ridx_neg(int h, long long i, int cap) {
+    long long x = ((long long)h + i) % cap;
+    return (int)(x < 0 ? x + cap : x);
+  }
+  static constexpr int LINEAR = 0x7fffffff;
+
+  // pop min(want, size) from the front of a ring
+  __device__ int ring_pop_front(E* ring, int& h, int& n, E* dst, int want) {
+    const int c = min(want, n);
+    const int cap = p.l1cap;
+    for (int i = lane; i < c; i += 32) dst[i] = ring[ridx(h, i, cap)];
+    h = ridx(h, c, cap);
+    n -= c;
+    __syncwarp();
+    return c;
+  }
+
+  // append spill[from..to) (predicate-filtered, stable) to the ring tail; returns count
+  __device__ void ring_append(E* ring, int h, int& n, const E* src, int i0, int cnt) {
+    const int cap = p.l1cap;
+    for (int i = lane; i < cnt; i += 32) ring[ridx(h, n + i, cap)] = src[i0 + i];
+    n += cnt;
+    __syncwarp();
+  }
+
+  // L1 Vector write (l1.py:116-129): append, evict the front over capacity, flush all
+  // after every wb write invocations.
+  __device__ void l1_vector_write(int ns) {
+    const int cap = p.l1cap;
+    const int total = n1 + ns;
+    const int evict = max(0, total - cap);
+    const int er = min(evict, n1), es = evict - er;
+    if (er) { write_back(l1a, h1, er, cap); h1 = ridx(h1, er, cap); n1 -= er; }
+    if (es) write_back(spill, 0, es, LINEAR);
+    ring_append(l1a, h1, n1, spill, es, ns - es);
+    count(M_L1E, (unsigned long long)ns);
+    count(M_L1D, (unsigned long long)evict);
+    if (p.wb > 0 && ++wcount >= p.wb) {
+      count(M_L1D, (unsigned long long)n1);
+      write_back(l1a, h1, n1, cap);
+      h1 = 0;
+      n1 = 0;
+      wcount = 0;
+      count(M_FLUSH, 1);
+    }
+  }
+
+  // stable in-place compaction of flagged spill elements to spill[0..); returns count
+  // (the caller computed `flag(i)` per element; write index never passes read index)
+  // L1 Filter write (l1.py:213-230): admit d <= F, reject to L2 tracking reject_min,
+  // evict the front over capacity.
+  __device__ void l1_filter_write(int ns) {
+    const int cap = p.l1cap;
+    int A = 0;
+    S rmin = rej_min;
+    for (int o = 0; o < ns; o += 32) {
+      const bool has = o + lane < ns;
+      S d = has ? spill[o + lane].d : (S)0;
+      const bool adm = has && d <= thr;
+      A += __popc(__ballot_sync(FULL, adm));
+      S rd = (has && !adm) ? d : (S)Tr::INF;
+#pragma unroll
+      for (int k = 16; k > 0; k >>= 1) {
+        S t = __shfl_xor_sync(FULL, rd, k);
+        rd = t < rd ? t : rd;
+      }
+      if (__any_sync(FULL, has && !adm)) {
+        has_rej = true;
+        if (rd < rmin) rmin = rd;
+      }
+    }
+    rej_min = rmin;
+    const int total = n1 + A;
+    const int evict = max(0, total - cap);
+    const int er = min(evict, n1), en = evict - er;
+    if (er) { write_back(l1a, h1, er, cap); h1 = ridx(h1, er, cap); n1 -= er; }
+    // second pass: admitted beyond the first `en` go to the ring; rejects and the
+    // first `en` admitted are compacted to the spill front and written back
+    int adm_seen = 0, back = 0;
+    for (int o = 0; o < ns; o += 32) {
+      const bool has = o + lane < ns;
+      E x;
+      if (has) x = spill[o + lane];
+      __syncwarp();
+      const bool adm = has && x.d <= thr;
+      const unsigned am = __ballot_sync(FULL, adm);
+      const int arank = adm_seen + __popc(am & lanemask_lt());
+      const bool to_ring = adm && arank >= en;
+      const bool to_back = has && !to_ring;
+      const unsigned rm = __ballot_sync(FULL, to_ring);
+      const unsigned bm = __ballot_sync(FULL, to_back);
+      if (to_ring) l1a[ridx(h1, n1 + __popc(rm & lanemask_lt()), cap)] = x;
+      if (to_back) spill[back + __popc(bm & lanemask_lt())] = x;
+      n1 += __popc(rm);
+      back += __popc(bm);
+      adm_seen += __popc(am);
+      __syncwarp();
+    }
+    write_back(spill, 0, back, LINEAR);
+    count(M_L1E, (unsigned long long)A);
+    count(M_L1D, (unsigned long long)evict);
+  }
+
+  // L1 NearFar write (l1.py:157-177): partition by d < NF; over capacity evict
+  // far-front first, then near-front.
+  __device__ void l1_nearfar_write(int ns) {
+    const int cap = p.l1cap;
+    int Nn = 0;
+    for (int o = 0; o < ns; o += 32) {
+      const bool has = o + lane < ns;
+      const bool nr = has && spill[o + lane].d < thr;
+      Nn += __popc(__ballot_sync(FULL, nr));
+    }
+    const int Nf = ns - Nn;
+    const int total = n1 + n2 + ns;
+    const int over = max(0, total - cap);
+    const int ef = min(over, n2 + Nf);
+    const int efr = min(ef, n2), efn = ef - efr;
+    const int en = over - ef;
+    const int enr = min(en, n1), enn = en - enr;
+    if (efr) { write_back(l1b, h2, efr, cap); h2 = ridx(h2, efr, cap); n2 -= efr; }
+    if (enr) { write_back(l1a, h1, enr, cap); h1 = ridx(h1, enr, cap); n1 -= enr; }
+    int ns_seen = 0, fs_seen = 0, back = 0;
+    for (int o = 0; o < ns; o += 32) {
+      const bool has = o + lane < ns;
+      E x;
+      if (has) x = spill[o + lane];
+      __syncwarp();
+      const bool nr = has && x.d < thr;
+      const bool fr = has && !nr;
+      const unsigned nm = __ballot_sync(FULL, nr), fm = __ballot_sync(FULL, fr);
+      const int nrk = ns_seen + __popc(nm & lanemask_lt());
+      const int frk = fs_seen + __popc(fm & lanemask_lt());
+      const bool to_near = nr && nrk >= enn;
+      const bool to_far = fr && frk >= efn;
+      const bool to_back = has && !to_near && !to_far;
+      const unsigned tn = __ballot_sync(FULL, to_near), tf = __ballot_sync(FULL, to_far),
+                     tb = __ballot_sync(FULL, to_back);
+      if (to_near) l1a[ridx(h1, n1 + __popc(tn & lanemask_lt()), cap)] = x;
+      if (to_far) l1b[ridx(h2, n2 + __popc(tf & lanemask_lt()), cap)] = x;
+      if (to_back) spill[back + __popc(tb & lanemask_lt())] = x;
+      n1 += __popc(tn);
+      n2 += __popc(tf);
+      back += __popc(tb);
+      ns_seen += __popc(nm);
+      fs_seen += __popc(fm);
+      __syncwarp();
+    }
+    write_back(spill, 0, back, LINEAR);
+    count(M_L1E, (unsigned long long)ns);
+    count(M_L1D, (unsigned long long)over);
+  }
+
+  // L1 SLF write (l1.py:263-274): head distance snapshot; shorter -> push front
+  // (reversing arrival order), else push back; over capacity pop from the tail.
+  __device__ void l1_slf_write(int ns) {
+    const int cap = p.l1cap;
+    S hd = (S)Tr::INF;
+    if (n1 > 0) hd = l1a[h1].d;
+    int pf = 0;
+    for (int o = 0; o < ns; o += 32) {
+      const bool has = o + lane < ns;
+      pf += __popc(__ballot_sync(FULL, has && spill[o + lane].d < hd));
+    }
+    const int total = pf + n1 + ns - pf;
+    const int over = max(0, total - cap);
+    // old content with deque index pf + j >= cap is evicted (ring tail); copy it out
+    // before front pushers reuse those slots
+    const int keep_old = max(0, min(n1, cap - pf));
+    const int eo = n1 - keep_old;
+    if (eo) write_back(l1a, ridx(h1, keep_old, cap), eo, cap);
+    const int sb = max(0, cap - pf - n1);  // surviving back pushers
+    int f_seen = 0, b_seen = 0, back = 0;
+    for (int o = 0; o < ns; o += 32) {
+      const bool has = o + lane < ns;
+      E x;
+      if (has) x = spill[o + lane];
+      __syncwarp();
+      const bool fr = has && x.d < hd;
+      const bool bk = has && !fr;
+      const unsigned fm = __ballot_sync(FULL, fr), bm = __ballot_sync(FULL, bk);
+      const int frk = f_seen + __popc(fm & lanemask_lt());
+      const int brk = b_seen + __popc(bm & lanemask_lt());
+      const bool f_keep = fr && (pf - 1 - frk) < cap;
+      const bool b_keep = bk && brk < sb;
+      const bool to_back = has && !f_keep && !b_keep;
+      const unsigned tb = __ballot_sync(FULL, to_back);
+      if (f_keep) l1a[ridx_neg(h1, -1 - (long long)frk, cap)] = x;
+      if (b_keep) l1a[ridx(h1, n1 + brk, cap)] = x;
+      if (to_back) spill[back + __popc(tb & lanemask_lt())] = x;
+      back += __popc(tb);
+      f_seen += __popc(fm);
+      b_seen += __popc(bm);
+      __syncwarp();
+    }
+    h1 = ridx_neg(h1, -(long long)min(pf, cap), cap);
+    n1 = min(total, cap);
+    write_back(spill, 0, back, LINEAR);
+    count(M_L1E, (unsigned long long)ns);
+    count(M_L1D, (unsigned long long)over);
+  }
+
+  __device__ void l1_write(int ns) {
+    switch (p.l1type) {
+      case L1K_VECTOR: l1_vector_write(ns); break;
+      case L1K_NEAR_FAR: l1_nearfar_write(ns); break;
+      case L1K_FILTER: l1_filter_write(ns); break;
+      default: l1_slf_write(ns); break;
+    }
+  }
+
+  // L1 reads (l1.py:131-136, 179-189, 232-242, 276-280)
+  __device__ int l1_read(E* dst, int want) {
+    const int cap = p.l1cap;
+    if (p.l1type == L1K_NEAR_FAR) {
+      if (n1 == 0 && n2 > 0) {
+        S mn = (S)Tr::INF;
+        for (int i = lane; i < n2; i += 32) {
+          const S d = l1b[ridx(h2, i, cap)].d;
+          mn = d < mn ? d : mn;
+        }
+#pragma unroll
+        for (int k = 16; k > 0; k >>= 1) {
+          S t = __shfl_xor_sync(FULL, mn, k);
+          mn = t < mn ? t : mn;
+        }
+        thr = Tr::add_thr(mn, (S)p.delta_nf_s);
+        // stable repartition of far (near is empty: restart it at slot 0)
+        h1 = 0;
+        int kf = 0;
+        for (int o = 0; o < n2; o += 32) {
+          const bool has = o + lane < n2;
+          E x;
+          if (has) x = l1b[ridx(h2, o + lane, cap)];
+          __syncwarp();
+          const bool nr = has && x.d < thr;
+          const bool fr = has && !nr;
+          const unsigned nm = __ballot_sync(FULL, nr), fm = __ballot_sync(FULL, fr);
+          if (nr) l1a[n1 + __popc(nm & lanemask_lt())] = x;
+          if (fr) l1b[ridx(h2, kf + __popc(fm & lanemask_lt()), cap)] = x;
+          n1 += __popc(nm);
+          kf += __popc(fm);
+          __syncwarp();
+        }
+        n2 = kf;
+      }
+      return ring_pop_front(l1a, h1, n1, dst, want);
+    }
+    if (p.l1type == L1K_FILTER && n1 == 0) {
+      if (has_rej) {
+        thr = Tr::add_thr(rej_min, (S)p.filter_f_s);
+        rej_min = (S)Tr::INF;
+        has_rej = false;
+      }
+      return 0;
+    }
+    return ring_pop_front(l1a, h1, n1, dst, want);
+  }
+
+  // ============================================================ cascade write
+  // compose.py:56-77: L0.write; a full target lane triggers a full transfer of L0 plus
+  // the unplaced remainder into L1; L1's write-back goes through to L2.
+  __device__ void cascade_write(const E* src, int k) {
+    const bool has = lane < k;
+    E b;
+    if (has) b = src[lane];
+    const bool isfull = lane < L && l0n >= p.l0cap;
+    const unsigned fullmask = __ballot_sync(FULL, isfull);
+    const int t = (wc + lane) % L;
+    const bool fi = has && ((fullmask >> t) & 1u);
+    const unsigned fm = __ballot_sync(FULL, fi);
+    const int f = fm ? __ffs(fm) - 1 : k;
+    const int si = (lane - wc + L) % L;
+    const uint32_t gv = __shfl_sync(FULL, b.v, si & 31);
+    const S gd = __shfl_sync(FULL, b.d, si & 31);
+    if (lane < L && si < f) l0_push(gv, gd);
+    count(M_L0E, (unsigned long long)f);
+    if (f == k) {
+      wc = (wc + k) % L;
+      l0size += k;
+      return;
+    }
+    const int before = l0size;
+    int ns = l0_drain(spill);
+    if (has && lane >= f) spill[ns + lane - f] = b;
+    ns += k - f;
+    wc = (wc + f) % L;
+    l0size = 0;
+    count(M_L0D, (unsigned long long)(before + f));
+    __syncwarp();
+    l1_write(ns);
+  }
+
+  __device__ void flush_out(bool all) {
+    int d = 0;
+    while (outn - d >= L) {
+      cascade_write(outs + d, L);
+      d += L;
+    }
+    if (all && outn - d > 0) {
+      cascade_write(outs + d, outn - d);
+      d = outn;
+    }
+    const int rem = outn - d;
+    if (d > 0 && rem > 0) {
+      E tmp;
+      if (lane < rem) tmp = outs[d + lane];
+      __syncwarp();
+      if (lane < rem) outs[lane] = tmp;
+    }
+    outn = rem;
+    __syncwarp();
+  }
+
+  // ============================================================ relaxation
+  // engine.py:201-220 per edge: nd = dist[u] + w; if nd < dist[v] and atomic-min
+  // improves (core.py:205-213): emit (v, nd).
+  __device__ void relax_slots(bool (&act)[U], const unsigned long long (&kk)[U], const S (&du)[U]) {
+    uint32_t v[U];
+    S nd[U];
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (act[j]) {
+        const uint2 a = __ldg(p.adj + kk[j]);
+        v[j] = a.x;
+        nd[j] = Tr::add(du[j], p.unit ? 1u : a.y, dist_ovf);
+        ++c;
+        if (nd[j] == (S)Tr::INF) act[j] = false;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (act[j]) act[j] = nd[j] < ldcg_dist(dist + v[j]);
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (act[j]) act[j] = nd[j] < atomicMin(dist + v[j], nd[j]);
+    const int tot = __reduce_add_sync(FULL, c);
+    int upd = 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const unsigned m = __ballot_sync(FULL, act[j]);
+      if (act[j]) {
+        E e;
+        e.v = v[j];
+        e.d = nd[j];
+        outs[outn + __popc(m & lanemask_lt())] = e;
+      }
+      outn += __popc(m);
+      upd += __popc(m);
+    }
+    count(M_RELAX, (unsigned long long)tot);
+    count(M_UPD, (unsigned long long)upd);
+    __syncwarp();
+    if (outn >= L) flush_out(false);
+  }
+
+  // the whole warp strides one edge list (engine.py:212-220 "big" tier, hub chunks)
+  __device__ void relax_range(unsigned long long lo, unsigned long long hi, S du) {
+    const S dus[U] = {du, du, du, du};
+    for (unsigned long long k0 = lo; k0 < hi; k0 += 32 * U) {
+      bool act[U];
+      unsigned long long kk[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        kk[j] = k0 + (unsigned long long)(j * 32 + lane);
+        act[j] = kk[j] < hi;
+      }
+      relax_slots(act, kk, dus);
+    }
+  }
+
+  __device__ void push_hub(uint32_t u, S du, unsigned long long lo, unsigned long long hi) {
+    const unsigned long long ch = p.hub_chunk;
+    const unsigned long long nch = (hi - lo + ch - 1) / ch;
+    unsigned long long t = 0;
+    if (lane == 0) {
+      t = atomicAdd(p.ctl + C_HUB_WP, nch);
+      atomicAdd(p.ctl + C_HUB_ITEMS, nch);
+    }
+    t = __shfl_sync(FULL, t, 0);
+    const unsigned long long cap = p.hub_mask + 1;
+    for (unsigned long long q = lane; q < nch; q += 32) {
+      const unsigned long long tk = t + q, slot = tk & p.hub_mask;
+      unsigned long long t0 = 0;
+      int spins = 0;
+      bool ok = true;
+      while (ld_acquire(p.hub_seq + slot) != tk) {
+        if (++spins % 64 == 0) {
+          if (stopped()) { ok = false; break; }
+          unsigned long long now = globaltimer_ns();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > p.spin_timeout_ns) {
+            raise_error(ERR_HUB_OVERFLOW, 0, slot, t, cap);
+            ok = false;
+            break;
+          }
+        }
+        __nanosleep(64);
+      }
+      if (!ok) break;
+      HubItem it;
+      it.lo = lo + q * ch;
+      it.hi = min(hi, lo + (q + 1) * ch);
+      it.du = (unsigned long long)du;
+      it.u = u;
+      it.pad = 0;
+      p.hub_data[slot] = it;
+      __threadfence();
+      st_release(p.hub_seq + slot, tk + 1);
+    }
+    __syncwarp();
+  }
+
+  // Claim one hub item if any; returns true and processes it.
+  __device__ bool hub_try() {
+    unsigned long long r = 0;
+    int got = 0;
+    if (lane == 0) {
+      unsigned long long* rpp = p.ctl + C_HUB_RP;
+      unsigned long long* wpp = p.ctl + C_HUB_WP;
+      r = ld_relaxed(rpp);
+      unsigned long long w = ld_relaxed(wpp);
+      while (r < w) {
+        unsigned long long old = atomicCAS(rpp, r, r + 1);
+        if (old == r) { got = 1; break; }
+        r = old;
+        if (r >= w) w = ld_relaxed(wpp);
+      }
+    }
+    got = __shfl_sync(FULL, got, 0);
+    if (!got) return false;
+    r = __shfl_sync(FULL, r, 0);
+    const unsigned long long slot = r & p.hub_mask;
+    HubItem it;
+    int ok = 1;
+    if (lane == 0) {
+      while (ld_acquire(p.hub_seq + slot) != r + 1) {
+        if (stopped()) { ok = 0; break; }
+        __nanosleep(64);
+      }
+      if (ok) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.hub_data + slot);
+        uint4 a = __ldcg(src), b = __ldcg(src + 1);
+        it.lo = ((unsigned long long)a.y << 32) | a.x;
+        it.hi = ((unsigned long long)a.w << 32) | a.z;
+        it.du = ((unsigned long long)b.y << 32) | b.x;
+        it.u = b.z;
+        st_release(p.hub_seq + slot, r + p.hub_mask + 1);
+      }
+    }
+    if (!__shfl_sync(FULL, ok, 0)) return true;
+    it.lo = __shfl_sync(FULL, it.lo, 0);
+    it.hi = __shfl_sync(FULL, it.hi, 0);
+    it.du = __shfl_sync(FULL, it.du, 0);
+    it.u = __shfl_sync(FULL, it.u, 0);
+    local_done += 1;
+    S du = (S)it.du;
+    const S cur = ldcg_dist(dist + it.u);
+    if (p.dup && du > cur) return true;  // stale hub item (engine.py:190 analogue)
+    if (cur < du) du = cur;
+    relax_range(it.lo, it.hi, du);
+    return true;
+  }
+
+  // engine.py:171-227 for one batch in shared memory
+  __device__ void relax_batch(int nb) {
+    for (int base = 0; base < nb; base += 32) {
+      const int i = base + lane;
+      bool valid = i < nb;
+      E e;
+      S du = (S)Tr::INF;
+      unsigned long long lo = 0, hi = 0;
+      if (valid) {
+        e = batch[i];
+        const S cur = ldcg_dist(dist + e.v);
+        if (p.dup && e.d > cur) valid = false;  // stale duplicate (engine.py:190-191)
+        du = e.d < cur ? e.d : cur;
+      }
+      const unsigned vm = __ballot_sync(FULL, valid);
+      count(M_SETTLED, (unsigned long long)__popc(vm));
+      if (valid) {
+        lo = __ldg(p.off + e.v);
+        hi = __ldg(p.off + e.v + 1);
+      }
+      // hub tier: split huge lists into shared edge-range items
+      unsigned hm = __ballot_sync(FULL, valid && (hi - lo) > p.hub_thresh);
+      while (hm) {
+        const int l = __ffs(hm) - 1;
+        const uint32_t hu = __shfl_sync(FULL, e.v, l);
+        const S hdu = __shfl_sync(FULL, du, l);
+        const unsigned long long hlo = __shfl_sync(FULL, lo, l);
+        const unsigned long long hhi = __shfl_sync(FULL, hi, l);
+        push_hub(hu, hdu, hlo + p.hub_chunk, hhi);
+        if (lane == l) hi = lo + p.hub_chunk;
+        hm &= hm - 1;
+      }
+      const unsigned long long deg = hi - lo;
+      const bool big = valid && deg > (unsigned long long)p.th_v;
+      const bool small = valid && !big;
+      // small lists: flattened, load-balanced across lanes (warp scan + search)
+      const int ds = small ? (int)deg : 0;
+      const int incl = warp_incl_scan(ds, lane);
+      const int total = __shfl_sync(FULL, incl, 31);
+      const int excl = incl - ds;
+      for (int e0 = 0; e0 < total; e0 += 32 * U) {
+        bool act[U];
+        unsigned long long kk[U];
+        S dus[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int idx = e0 + j * 32 + lane;
+          int o = 0;
+#pragma unroll
+          for (int s = 16; s >= 1; s >>= 1) {
+            const int probe = __shfl_sync(FULL, incl, o + s - 1);
+            if (probe <= idx) o += s;
+          }
+          const unsigned long long olo = __shfl_sync(FULL, lo, o);
+          const int oex = __shfl_sync(FULL, excl, o);
+          dus[j] = __shfl_sync(FULL, du, o);
+          act[j] = idx < total;
+          kk[j] = olo + (unsigned long long)(idx - oex);
+        }
+        relax_slots(act, kk, dus);
+      }
+      // big lists: the whole warp walks each one
+      unsigned bm = __ballot_sync(FULL, big);
+      while (bm) {
+        const int l = __ffs(bm) - 1;
+        relax_range(__shfl_sync(FULL, lo, l), __shfl_sync(FULL, hi, l), __shfl_sync(FULL, du, l));
+        bm &= bm - 1;
+      }
+    }
+    flush_out(true);
+  }
+
+  // ============================================================ read cascade
+  // compose.py:30-54. Returns >0 batch size, -1 when a hub item was processed, 0 on a
+  // full miss.
+  __device__ int read_cascade() {
+    if (l0size > 0) {
+      const int c = l0_read(batch, L);
+      count(M_L0D, (unsigned long long)c);
+      return c;
+    }
+    const int c1 = l1_read(batch, L);
+    if (c1 > 0) {
+      count(M_L1D, (unsigned long long)c1);
+      return c1;
+    }
+    if (hub_try()) return -1;
+    return l2_read(batch);
+  }
+
+  __device__ void run() {
+    int backoff = 0;
+    for (;;) {
+      if (stopped()) break;
+      const int c = read_cascade();
+      if (c > 0) {
+        relax_batch(c);
+        backoff = 0;
+        continue;
+      }
+      if (c < 0) {
+        flush_out(true);
+        backoff = 0;
+        continue;
+      }
+      // full miss: flush local_done (l2.py:56-62)
+      if (local_done) {
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(p.ctl + C_DONE, local_done);
+          met[M_L2A] += 1;
+        }
+        local_done = 0;
+        __syncwarp();
+      }
+      __nanosleep(32u << min(backoff, 5));
+      ++backoff;
+    }
+    // exit: metric shard + audit evidence
+    if (__any_sync(FULL, dist_ovf) && lane == 0) atomicOr(p.ctl + C_DIST_OVF, 1ull);
+    const int l1size = n1 + n2;
+    if (lane == 0) {
+      for (int f = 0; f < M_COUNT; ++f) p.metrics[(size_t)gid * M_COUNT + f] = met[f];
+      if (l0size + l1size + outn) atomicAdd(p.ctl + C_LOCAL_NONEMPTY, (unsigned long long)(l0size + l1size + outn));
+    }
+  }
+};
+
+// K2: manager warp (engine.py:152-169): reserve == done on three consecutive polls.
+static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
+  int k = 0;
+  for (;;) {
+    if (p.host_abort && lane == 0 && ld_sys_u32(p.host_abort) != 0u) {
+      atomicCAS(p.ctl + C_ERR, 0ull, (unsigned long long)ERR_ABORT);
+      __threadfence();
+      st_release(p.ctl + C_STOP, 1ull);
+    }
+    __syncwarp();
+    if (ld_relaxed(p.ctl + C_STOP) != 0ull) break;
+    const unsigned long long d = ld_acquire(p.ctl + C_DONE);
+    unsigned long long r = 0;
+    for (int i = lane; i < p.nrings; i += 32) r += ld_relaxed(p.ptrs + (size_t)i * 32);
+    for (int i = lane; i < p.pnum; i += 32) r += ld_relaxed(p.hwc + (size_t)i * 16);
+    if (lane == 0) r += ld_relaxed(p.ctl + C_HUB_WP);
+    r = warp_sum_u64(r);
+    k = (d == r) ? k + 1 : 0;
+    if (k >= 3) {
+      if (lane == 0) st_release(p.ctl + C_STOP, 1ull);
+      break;
+    }
+    __nanosleep(256);
+  }
+}
+
+template <int K, int L2K, int CM>
+__global__ void __launch_bounds__(256) mlmq_persistent_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (gid > p.G) return;
+  if (gid == p.G) {
+    manager_loop(p, lane);
+    return;
+  }
+  Worker<K, L2K, CM> w(p, smem + (size_t)warp * p.smem_per_warp, gid, lane);
+  w.run();
+}
+
+}  // namespace mlmq

@@ -1,0 +1,798 @@
+// mlmq_api.cu — the C ABI of include/mlmq.h: graph upload, workspace management,
+// solve orchestration (K3 init -> K1/K2 persistent kernel -> K5 audit), the host
+// watchdog, error mapping, features and reachability.
+//
+// Replaces the body of sssp_solve (pkg/src/mlq_sssp/engine.py:245-297): _Run
+// construction (:109-125), bootstrap (compose.py:92-101), worker/manager threads
+// (:260-265), watchdog (:267-279), audit (:229-242) and metric merge (:285-297).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/mlmq.h"
+#include "kernels/aux_kernels.cuh"
+#include "kernels/common.cuh"
+
+namespace mlmq {
+
+const void* kernel_for_dk0(int l2k, int cm);
+const void* kernel_for_dk1(int l2k, int cm);
+const void* kernel_for_dk2(int l2k, int cm);
+
+static thread_local char g_err[1024] = "";
+
+void set_last_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+}  // namespace mlmq
+
+using namespace mlmq;
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t _e = (call);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      set_last_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__, \
+                     __LINE__, cudaGetErrorString(_e));                              \
+      return MLMQ_ECUDA;                                                             \
+    }                                                                                \
+  } while (0)
+
+namespace {
+
+constexpr int kWarpsPerBlockMax = 8;
+constexpr int kOutCap = 32 * 4 + 32;
+constexpr int kAuditWords = 14;
+
+struct Workspace {
+  int es = 0, bs = 0, nrings = 0, nheaps = 0;
+  unsigned long long bn = 0, hcap = 0, hub_cap = 0;
+  unsigned long long* seq = nullptr;
+  uint32_t* cnt = nullptr;
+  void* data = nullptr;
+  unsigned long long* ptrs = nullptr;
+  uint32_t* hlock = nullptr;
+  unsigned long long* hsize = nullptr;
+  unsigned long long* hwc = nullptr;
+  void* hnodes = nullptr;
+  uint32_t* hcnt = nullptr;
+  unsigned long long* hub_seq = nullptr;
+  HubItem* hub_data = nullptr;
+  bool dirty = true;
+  size_t bytes = 0;
+};
+
+void ws_free(Workspace& w) {
+  cudaFree(w.seq);
+  cudaFree(w.cnt);
+  cudaFree(w.data);
+  cudaFree(w.ptrs);
+  cudaFree(w.hlock);
+  cudaFree(w.hsize);
+  cudaFree(w.hwc);
+  cudaFree(w.hnodes);
+  cudaFree(w.hcnt);
+  cudaFree(w.hub_seq);
+  cudaFree(w.hub_data);
+  w = Workspace();
+}
+
+unsigned long long next_pow2(unsigned long long x) {
+  unsigned long long p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+struct mlmq_graph {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  unsigned long long n = 0, m = 0;
+  int wkind = MLMQ_W_U32;
+  unsigned long long* d_off = nullptr;
+  uint2* d_adj = nullptr;
+  void* d_dist = nullptr;               // n x 8 bytes
+  unsigned long long* d_dist64 = nullptr;  // widen buffer
+  unsigned long long* d_ctl = nullptr;
+  unsigned long long* d_audit = nullptr;
+  unsigned long long* d_metrics = nullptr;
+  unsigned long long metrics_cap = 0;
+  unsigned long long* d_scratch = nullptr;  // 16 words for features / reach
+  uint32_t* h_abort = nullptr;
+  uint32_t* d_abort = nullptr;
+  Workspace ws;
+  int last_dk = -1;
+  std::mutex mu;
+};
+
+namespace {
+
+const void* kernel_for(int dk, int l2k, int cm) {
+  switch (dk) {
+    case DK_U32: return kernel_for_dk0(l2k, cm);
+    case DK_U64: return kernel_for_dk1(l2k, cm);
+    default: return kernel_for_dk2(l2k, cm);
+  }
+}
+
+int l2_kind(int l2_type) {
+  switch (l2_type) {
+    case MLMQ_L2_FIFO: return L2K_FIFO;
+    case MLMQ_L2_BUCKET: return L2K_BUCKET;
+    default: return L2K_HEAP;
+  }
+}
+
+int validate(const mlmq_config_t* c) {
+  if (c->l1_type < 0 || c->l1_type > 3) { set_last_error("unknown l1_type code %d", c->l1_type); return MLMQ_EINVAL; }
+  if (c->l2_type < 0 || c->l2_type > 3) { set_last_error("unknown l2_type code %d", c->l2_type); return MLMQ_EINVAL; }
+  if (c->l0_capacity < 1 || c->l0_capacity > 16) { set_last_error("l0_capacity must be in [1, 16] on the GPU engine (got %d)", c->l0_capacity); return MLMQ_EINVAL; }
+  if (c->l1_capacity < 1) { set_last_error("l1 capacity must be >= 1"); return MLMQ_EINVAL; }
+  if (c->wb < 0) { set_last_error("wb must be >= 0 (0 disables periodic flushing)"); return MLMQ_EINVAL; }
+  if (c->lanes_per_group < 1 || c->lanes_per_group > 32) { set_last_error("lanes_per_group must be in [1, 32] on the GPU engine (got %d)", c->lanes_per_group); return MLMQ_EINVAL; }
+  if (c->th_v < 0) { set_last_error("th_v must be >= 0"); return MLMQ_EINVAL; }
+  if (c->block_size < 1 || c->block_size > 4096 || c->block_num < 1) { set_last_error("block_size must be in [1, 4096] and block_num >= 1"); return MLMQ_EINVAL; }
+  if (c->bmax < 1 || c->bnum < 1 || c->bmax > 4096) { set_last_error("bmax and bnum must be >= 1 (bmax <= 4096)"); return MLMQ_EINVAL; }
+  if (c->bnum > c->bmax) { set_last_error("bnum must not exceed bmax"); return MLMQ_EINVAL; }
+  if (c->node_batch < 1) { set_last_error("node_batch must be >= 1"); return MLMQ_EINVAL; }
+  if (c->l2_type == MLMQ_L2_BUCKET && !(c->delta > 0)) { set_last_error("bucket delta must be > 0"); return MLMQ_EINVAL; }
+  if (c->l2_type == MLMQ_L2_MULTI && c->pnum < 1) { set_last_error("pnum must be >= 1"); return MLMQ_EINVAL; }
+  return MLMQ_OK;
+}
+
+struct LaunchShape {
+  const void* fn = nullptr;
+  int dk = 0, l2k = 0, cm = 4;
+  int smem_per_warp = 0, wpb = 0;
+  int batch_cap = 0, spill_cap = 0;
+  int max_groups = 0;
+};
+
+int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) {
+  s->dk = dk;
+  s->l2k = l2_kind(c->l2_type);
+  s->cm = c->l0_capacity <= 4 ? 4 : 16;
+  s->fn = kernel_for(dk, s->l2k, s->cm);
+  const int es = dk == DK_U64 ? 16 : 8;
+  const int L = c->lanes_per_group;
+  s->batch_cap = std::max(c->block_size, 32);
+  s->spill_cap = L * c->l0_capacity + L;
+  const int l1n = (c->l1_type == MLMQ_L1_NEAR_FAR ? 2 : 1) * c->l1_capacity;
+  long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n) + M_COUNT * 8;
+  bytes = (bytes + 15) / 16 * 16;
+  int max_smem_block = 0;
+  CK(cudaDeviceGetAttribute(&max_smem_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
+  if (bytes > max_smem_block) {
+    set_last_error("queue configuration needs %lld bytes of shared memory per group; the device allows %d (reduce l1 capacity or block_size)", bytes, max_smem_block);
+    return MLMQ_EINVAL;
+  }
+  s->smem_per_warp = (int)bytes;
+  s->wpb = (int)std::min<long long>(kWarpsPerBlockMax, max_smem_block / bytes);
+  static std::mutex attr_mu;
+  static std::unordered_set<const void*> attr_done;
+  {
+    std::lock_guard<std::mutex> lk(attr_mu);
+    if (!attr_done.count(s->fn)) {
+      CK(cudaFuncSetAttribute(s->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_block));
+      attr_done.insert(s->fn);
+    }
+  }
+  int bps = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, s->fn, s->wpb * 32, (size_t)s->wpb * bytes));
+  if (bps < 1) { set_last_error("persistent kernel cannot be made resident for this configuration"); return MLMQ_EINVAL; }
+  s->max_groups = bps * g->sm_count * s->wpb - 1;
+  return MLMQ_OK;
+}
+
+int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& sh, unsigned long long hub_chunk) {
+  Workspace need;
+  need.es = sh.dk == DK_U64 ? 16 : 8;
+  need.bs = c->block_size;
+  const unsigned long long n = g->n;
+  if (sh.l2k == L2K_HEAP) {
+    need.nrings = 0;
+    need.bn = 1;
+    need.nheaps = c->l2_type == MLMQ_L2_MULTI ? c->pnum : 1;
+    unsigned long long total = std::max<unsigned long long>(65536ull, 4ull * n + 4096ull);
+    need.hcap = std::max<unsigned long long>(256ull, total / (unsigned long long)need.nheaps);
+  } else {
+    need.nrings = sh.l2k == L2K_BUCKET ? c->bmax : 1;
+    const unsigned long long slots = 8ull * n / (unsigned long long)c->block_size + 16384ull;
+    unsigned long long per = sh.l2k == L2K_BUCKET ? slots / 8 + 1024 : slots;
+    need.bn = next_pow2(std::max<unsigned long long>((unsigned long long)c->block_num, per));
+    need.nheaps = 0;
+    need.hcap = 0;
+  }
+  need.hub_cap = next_pow2(2ull * g->m / hub_chunk + 4096ull);
+
+  Workspace& w = g->ws;
+  const bool fits = w.es == need.es && w.bs == need.bs && w.nrings == need.nrings &&
+                    w.nheaps == need.nheaps && w.bn >= need.bn && w.hcap >= need.hcap &&
+                    w.hub_cap >= need.hub_cap && w.ptrs != nullptr;
+  if (!fits) {
+    ws_free(w);
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const double budget = 0.7 * (double)free_b;
+    auto ring_bytes = [&](unsigned long long bn) {
+      return (double)need.nrings * (double)bn * ((double)need.bs * need.es + 12.0);
+    };
+    while (need.nrings && ring_bytes(need.bn) > budget && need.bn > (unsigned long long)c->block_num && need.bn > 1024) need.bn >>= 1;
+    if (need.nrings && ring_bytes(need.bn) > budget) {
+      set_last_error("L2 queue rings need %.1f GB; only %.1f GB of device memory is free", ring_bytes(need.bn) / 1e9, free_b / 1e9);
+      return MLMQ_ENOMEM;
+    }
+    const double heap_bytes = (double)need.nheaps * (double)need.hcap * (32.0 * need.es + 4.0);
+    if (heap_bytes > budget) {
+      need.hcap = std::max<unsigned long long>(64ull, (unsigned long long)(budget / ((double)need.nheaps * (32.0 * need.es + 4.0))));
+    }
+    const size_t nslots = (size_t)std::max(need.nrings, 1) * need.bn;
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](void** p, size_t b) {
+      if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(b, 256));
+      w.bytes += b;
+    };
+    w = need;
+    w.bytes = 0;
+    w.seq = nullptr;
+    alloc((void**)&w.seq, nslots * 8);
+    alloc((void**)&w.cnt, nslots * 4);
+    alloc(&w.data, need.nrings ? nslots * (size_t)need.bs * need.es : 256);
+    alloc((void**)&w.ptrs, (size_t)std::max(need.nrings, 1) * 32 * 8);
+    const size_t nh = (size_t)std::max(need.nheaps, 1);
+    alloc((void**)&w.hlock, nh * 32 * 4);
+    alloc((void**)&w.hsize, nh * 16 * 8);
+    alloc((void**)&w.hwc, nh * 16 * 8);
+    alloc(&w.hnodes, need.nheaps ? nh * need.hcap * 32 * need.es : 256);
+    alloc((void**)&w.hcnt, need.nheaps ? nh * need.hcap * 4 : 256);
+    alloc((void**)&w.hub_seq, need.hub_cap * 8);
+    alloc((void**)&w.hub_data, need.hub_cap * sizeof(HubItem));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ws_free(w);
+      set_last_error("device allocation of the queue workspace failed: %s", cudaGetErrorString(e));
+      return MLMQ_ENOMEM;
+    }
+    w.dirty = true;
+  }
+  if (w.dirty) {
+    const size_t nslots = (size_t)std::max(w.nrings, 1) * w.bn;
+    reset_queues_kernel<<<1024, 256, 0, g->stream>>>(w.seq, nslots, w.bn - 1, w.ptrs, std::max(w.nrings, 1),
+                                                      w.hub_seq, w.hub_cap, g->d_ctl, w.hlock, w.hsize, w.hwc,
+                                                      std::max(w.nheaps, 1));
+    CK(cudaGetLastError());
+    w.dirty = false;
+  }
+  return MLMQ_OK;
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// One attempt at a given distance kind.  Returns MLMQ_OK, an error, or 100 when the
+// optimistic u32 distances overflowed (caller re-runs in u64).
+int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, int dk,
+             mlmq_metrics_t* mo, uint64_t* gm, uint64_t gm_cap) {
+  LaunchShape sh;
+  int st = launch_shape(g, c, dk, &sh);
+  if (st) return st;
+  int G = c->num_groups > 0 ? c->num_groups : sh.max_groups;
+  if (G > sh.max_groups) {
+    set_last_error("num_groups=%d exceeds the %d groups the device keeps resident for this configuration", G, sh.max_groups);
+    return MLMQ_EINVAL;
+  }
+  const unsigned long long hub_chunk = c->hub_chunk > 0 ? (unsigned long long)c->hub_chunk : 2048ull;
+  if ((st = ensure_workspace(g, c, sh, hub_chunk))) return st;
+  if (g->metrics_cap < (unsigned long long)G) {
+    cudaFree(g->d_metrics);
+    g->d_metrics = nullptr;
+    g->metrics_cap = 0;
+    CK(cudaMalloc(&g->d_metrics, (size_t)G * M_COUNT * 8));
+    g->metrics_cap = G;
+  }
+  Workspace& w = g->ws;
+  KParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.off = g->d_off;
+  p.adj = g->d_adj;
+  p.n = g->n;
+  p.dist = g->d_dist;
+  p.source = source;
+  p.L = c->lanes_per_group;
+  p.l0cap = c->l0_capacity;
+  p.l1type = c->l1_type;
+  p.l1cap = c->l1_capacity;
+  p.wb = c->wb;
+  p.th_v = c->th_v;
+  p.dup = c->dup_elim;
+  p.unit = c->unit_weights || g->wkind == MLMQ_W_UNIT;
+  p.bs = c->block_size;
+  p.bmax = c->bmax;
+  p.bnum = c->bnum;
+  p.nb = std::min(c->node_batch, 32);
+  p.G = G;
+  if (dk == DK_F32) {
+    float nf = (float)c->delta_nf, ff = (float)c->filter_f;
+    uint32_t bnf, bff;
+    std::memcpy(&bnf, &nf, 4);
+    std::memcpy(&bff, &ff, 4);
+    p.delta_nf_s = bnf;
+    p.filter_f_s = bff;
+    p.delta_f = c->delta > 0 ? c->delta : 1.0;
+    p.delta_i = 1;
+  } else {
+    const double cap = dk == DK_U32 ? 4294967294.0 : 1.8e19;
+    p.delta_nf_s = (unsigned long long)std::min(std::max(c->delta_nf, 0.0), cap);
+    p.filter_f_s = (unsigned long long)std::min(std::max(c->filter_f, 0.0), cap);
+    p.delta_i = (unsigned long long)std::max(1.0, c->delta);
+    p.delta_f = (double)p.delta_i;
+  }
+  p.seq = w.seq;
+  p.cnt = w.cnt;
+  p.data = w.data;
+  p.ptrs = w.ptrs;
+  p.bn_mask = w.bn - 1;
+  p.nrings = w.nrings;
+  p.hlock = w.hlock;
+  p.hsize = w.hsize;
+  p.hwc = w.hwc;
+  p.hnodes = w.hnodes;
+  p.hcnt = w.hcnt;
+  p.hcap = w.hcap;
+  p.pnum = sh.l2k == L2K_HEAP ? w.nheaps : 0;
+  p.hub_seq = w.hub_seq;
+  p.hub_data = w.hub_data;
+  p.hub_mask = w.hub_cap - 1;
+  p.hub_chunk = hub_chunk;
+  p.hub_thresh = 2 * hub_chunk;
+  p.ctl = g->d_ctl;
+  p.host_abort = g->d_abort;
+  p.metrics = g->d_metrics;
+  const double spin = c->spin_timeout_s > 0 ? c->spin_timeout_s : 15.0;
+  p.spin_timeout_ns = (unsigned long long)(spin * 1e9);
+  p.smem_per_warp = sh.smem_per_warp;
+  p.batch_cap = sh.batch_cap;
+  p.out_cap = kOutCap;
+  p.spill_cap = sh.spill_cap;
+
+  *g->h_abort = 0;
+  const int blocks = (G + 1 + sh.wpb - 1) / sh.wpb;
+  const int init_blocks = (int)std::min<unsigned long long>(4ull * g->sm_count, (g->n + 255) / 256 + 1);
+  CK(cudaEventRecord(g->ev0, g->stream));
+  if (dk == DK_U64)
+    init_kernel<unsigned long long><<<init_blocks, 256, 0, g->stream>>>((unsigned long long*)g->d_dist, g->n, source, ~0ull, p, sh.l2k);
+  else
+    init_kernel<uint32_t><<<init_blocks, 256, 0, g->stream>>>((uint32_t*)g->d_dist, g->n, source,
+                                                              dk == DK_F32 ? 0x7f800000u : 0xFFFFFFFFu, p, sh.l2k);
+  CK(cudaGetLastError());
+  void* args[] = {(void*)&p};
+  CK(cudaLaunchCooperativeKernel(sh.fn, dim3(blocks), dim3(sh.wpb * 32), args,
+                                 (size_t)sh.wpb * sh.smem_per_warp, g->stream));
+  audit_kernel<<<1, 256, 0, g->stream>>>(p, g->d_audit);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(g->ev1, g->stream));
+
+  // host watchdog (engine.py:267-279)
+  const double wd = c->watchdog_s;
+  if (wd > 0) {
+    const double t0 = now_s();
+    bool aborted = false;
+    double abort_t = 0;
+    for (;;) {
+      cudaError_t q = cudaEventQuery(g->ev1);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) CK(q);
+      const double t = now_s();
+      if (!aborted && t - t0 > wd) {
+        *(volatile uint32_t*)g->h_abort = 1u;
+        aborted = true;
+        abort_t = t;
+      }
+      if (aborted && t - abort_t > 5.0) {
+        w.dirty = true;
+        set_last_error("worker failed to stop after abort");
+        return MLMQ_EENGINE;
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+  } else {
+    CK(cudaEventSynchronize(g->ev1));
+  }
+  unsigned long long au[kAuditWords];
+  CK(cudaMemcpy(au, g->d_audit, sizeof(au), cudaMemcpyDeviceToHost));
+  const unsigned long long err = au[6];
+  if (err == ERR_ABORT) {
+    w.dirty = true;
+    set_last_error("watchdog expired after %gs", wd);
+    return MLMQ_EENGINE;
+  }
+  if (err == ERR_OVERFLOW) {
+    w.dirty = true;
+    if (au[8] >= 1000000ull)
+      set_last_error("batch heap %llu lock stayed busy for %gs; the heap is likely too contended for this workload",
+                     au[8] - 1000000ull, spin);
+    else
+      set_last_error("ring slot %llu stayed busy for %gs (block_num=%llu, write_ptr=%llu, read_ptr=%llu); block_num is likely too small for this workload",
+                     au[9], spin, (unsigned long long)w.bn, au[10], au[11]);
+    return MLMQ_EOVERFLOW;
+  }
+  if (err == ERR_HEAP_OVERFLOW) {
+    w.dirty = true;
+    set_last_error("batch heap %llu is full (%llu of %llu nodes); raise node_batch or reduce pnum", au[8], au[9], au[10]);
+    return MLMQ_EOVERFLOW;
+  }
+  if (err == ERR_HUB_OVERFLOW) {
+    w.dirty = true;
+    set_last_error("hub work ring slot %llu stayed busy for %gs (capacity %llu)", au[9], spin, au[11]);
+    return MLMQ_EOVERFLOW;
+  }
+  if (err == 99) {
+    w.dirty = true;
+    set_last_error("queue ring state inconsistent at solve start");
+    return 101;  // caller resets and retries
+  }
+  if (au[7] && dk == DK_U32) return 100;
+  if (au[0] != au[1]) {
+    w.dirty = true;
+    set_last_error("termination audit failed: reserve=%llu done=%llu", au[1], au[0]);
+    return MLMQ_EENGINE;
+  }
+  if (au[5] != 0) {
+    w.dirty = true;
+    set_last_error("termination audit failed: groups hold %llu undelivered elements", au[5]);
+    return MLMQ_EENGINE;
+  }
+  if (au[2] || au[3] || au[4]) {
+    w.dirty = true;
+    set_last_error("termination audit failed: global queue not empty");
+    return MLMQ_EENGINE;
+  }
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+  std::vector<unsigned long long> hm((size_t)G * M_COUNT);
+  CK(cudaMemcpy(hm.data(), g->d_metrics, hm.size() * 8, cudaMemcpyDeviceToHost));
+  // the bootstrap write_through is charged to group 0 (compose.py:79-86, 92-101)
+  hm[M_L2E] += 1;
+  hm[M_L2A] += 1;
+  unsigned long long tot[M_COUNT] = {0};
+  for (int gi = 0; gi < G; ++gi)
+    for (int f = 0; f < M_COUNT; ++f) tot[f] += hm[(size_t)gi * M_COUNT + f];
+  if (mo) {
+    mo->relaxations = tot[M_RELAX];
+    mo->distance_updates = tot[M_UPD];
+    mo->l0_enqueues = tot[M_L0E];
+    mo->l0_dequeues = tot[M_L0D];
+    mo->l1_enqueues = tot[M_L1E];
+    mo->l1_dequeues = tot[M_L1D];
+    mo->l2_enqueues = tot[M_L2E];
+    mo->l2_dequeues = tot[M_L2D];
+    mo->l2_atomic_ops = tot[M_L2A];
+    mo->flushes = tot[M_FLUSH];
+    mo->settled_reads = tot[M_SETTLED];
+    mo->kernel_ms = ms;
+    mo->num_groups = (uint64_t)G;
+    mo->hub_items = au[12];
+    mo->dist_bits = dk == DK_U64 ? 64 : 32;
+  }
+  if (gm) {
+    const size_t cnt = std::min<size_t>((size_t)gm_cap, (size_t)G) * M_COUNT;
+    std::memcpy(gm, hm.data(), cnt * 8);
+  }
+  g->last_dk = dk;
+  return MLMQ_OK;
+}
+
+int copy_dist_u64(mlmq_graph* g, uint64_t* out) {
+  if (g->last_dk < 0) { set_last_error("no solve has run on this graph"); return MLMQ_EINVAL; }
+  if (g->last_dk == DK_U64) {
+    CK(cudaMemcpyAsync(out, g->d_dist, g->n * 8, cudaMemcpyDeviceToHost, g->stream));
+  } else {
+    if (!g->d_dist64) CK(cudaMalloc(&g->d_dist64, std::max<size_t>(8, g->n * 8)));
+    const int blocks = (int)std::min<unsigned long long>(8ull * g->sm_count, (g->n + 255) / 256 + 1);
+    widen_kernel<<<blocks, 256, 0, g->stream>>>((const uint32_t*)g->d_dist, g->d_dist64, g->n);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, g->d_dist64, g->n * 8, cudaMemcpyDeviceToHost, g->stream));
+  }
+  CK(cudaStreamSynchronize(g->stream));
+  return MLMQ_OK;
+}
+
+int solve(mlmq_graph* g, uint64_t source, const mlmq_config_t* c, void* dist_out, bool f32,
+          mlmq_metrics_t* mo, uint64_t* gm, uint64_t gm_cap) {
+  if (!g || !c) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  const double t0 = now_s();
+  std::lock_guard<std::mutex> lk(g->mu);
+  CK(cudaSetDevice(g->device));
+  if (source >= g->n) {
+    set_last_error("source %llu out of range for %llu vertices", (unsigned long long)source, g->n);
+    return MLMQ_EINVAL;
+  }
+  int st = validate(c);
+  if (st) return st;
+  const bool graph_f32 = g->wkind == MLMQ_W_F32;
+  if (f32 != graph_f32 && dist_out) {
+    set_last_error(graph_f32 ? "float-weight graph: use mlmq_sssp_f32" : "integer-weight graph: use mlmq_sssp");
+    return MLMQ_EINVAL;
+  }
+  int dk = graph_f32 ? DK_F32 : (c->dist_mode == MLMQ_DIST_U64 ? DK_U64 : DK_U32);
+  uint32_t reruns = 0;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    st = run_once(g, source, c, dk, mo, gm, gm_cap);
+    if (st == 100) { dk = DK_U64; reruns = 1; continue; }
+    if (st == 101) continue;
+    break;
+  }
+  if (st) return st;
+  if (dist_out) {
+    if (f32) {
+      CK(cudaMemcpyAsync(dist_out, g->d_dist, g->n * 4, cudaMemcpyDeviceToHost, g->stream));
+      CK(cudaStreamSynchronize(g->stream));
+    } else if ((st = copy_dist_u64(g, (uint64_t*)dist_out))) {
+      return st;
+    }
+  }
+  if (mo) {
+    mo->reruns = reruns;
+    mo->wall_time_us = (uint64_t)((now_s() - t0) * 1e6);
+  }
+  return MLMQ_OK;
+}
+
+__global__ void interleave_kernel(const uint32_t* col, const uint32_t* w, uint2* adj, unsigned long long m, int unit) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long k = tid; k < m; k += stride) adj[k] = make_uint2(col[k], unit ? 1u : w[k]);
+}
+
+}  // namespace
+
+extern "C" {
+
+int mlmq_abi_version(void) { return MLMQ_ABI_VERSION; }
+
+const char* mlmq_last_error(void) { return g_err; }
+
+int mlmq_device_count(int* out) {
+  if (!out) return MLMQ_EINVAL;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *out = 0;
+    set_last_error("no CUDA device: %s", cudaGetErrorString(e));
+    return MLMQ_ECUDA;
+  }
+  *out = n;
+  return MLMQ_OK;
+}
+
+int mlmq_device_info(int device, int* sm_count, size_t* free_bytes, size_t* total_bytes) {
+  CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  if (sm_count) *sm_count = sms;
+  size_t f = 0, t = 0;
+  CK(cudaMemGetInfo(&f, &t));
+  if (free_bytes) *free_bytes = f;
+  if (total_bytes) *total_bytes = t;
+  return MLMQ_OK;
+}
+
+int mlmq_graph_create(const uint64_t* row_offsets, const uint32_t* col, const void* w, int weight_kind,
+                      uint64_t n, uint64_t m, int device, mlmq_graph** out) {
+  if (!out || !row_offsets || (m && !col) || (m && weight_kind != MLMQ_W_UNIT && !w)) {
+    set_last_error("null argument");
+    return MLMQ_EINVAL;
+  }
+  if (n == 0 || n > 0xFFFFFFFFull) { set_last_error("vertex count must be in [1, 2^32-1]"); return MLMQ_EINVAL; }
+  if (row_offsets[n] != m) { set_last_error("row_offsets[n]=%llu does not match m=%llu", (unsigned long long)row_offsets[n], (unsigned long long)m); return MLMQ_EINVAL; }
+  *out = nullptr;
+  mlmq_graph* g = new mlmq_graph();
+  g->device = device;
+  g->n = n;
+  g->m = m;
+  g->wkind = weight_kind;
+  auto fail = [&](int code) {
+    mlmq_graph_destroy(g);
+    return code;
+  };
+#define CKG(call)                                                                          \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      set_last_error("CUDA error %s during graph upload: %s", cudaGetErrorName(_e),        \
+                     cudaGetErrorString(_e));                                              \
+      return fail(_e == cudaErrorMemoryAllocation ? MLMQ_ENOMEM : MLMQ_ECUDA);             \
+    }                                                                                      \
+  } while (0)
+  CKG(cudaSetDevice(device));
+  CKG(cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device));
+  int coop = 0;
+  CKG(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+  if (!coop) { set_last_error("device %d does not support cooperative launch", device); return fail(MLMQ_ECUDA); }
+  CKG(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  CKG(cudaEventCreate(&g->ev0));
+  CKG(cudaEventCreate(&g->ev1));
+  CKG(cudaMalloc(&g->d_off, (n + 1) * 8));
+  CKG(cudaMalloc(&g->d_adj, std::max<size_t>(8, m * 8)));
+  CKG(cudaMalloc(&g->d_dist, std::max<size_t>(8, n * 8)));
+  CKG(cudaMalloc(&g->d_ctl, C_WORDS * 8));
+  CKG(cudaMemset(g->d_ctl, 0, C_WORDS * 8));
+  CKG(cudaMalloc(&g->d_audit, kAuditWords * 8));
+  CKG(cudaMalloc(&g->d_scratch, 16 * 8));
+  CKG(cudaHostAlloc(&g->h_abort, 64, cudaHostAllocMapped));
+  *g->h_abort = 0;
+  CKG(cudaHostGetDevicePointer((void**)&g->d_abort, g->h_abort, 0));
+  CKG(cudaMemcpy(g->d_off, row_offsets, (n + 1) * 8, cudaMemcpyHostToDevice));
+  if (m) {
+    // interleave (col, weight) on the device in chunks: one 8-byte load per edge
+    const unsigned long long chunk = std::min<unsigned long long>(m, 1ull << 25);
+    uint32_t *dc = nullptr, *dw = nullptr;
+    CKG(cudaMalloc(&dc, chunk * 4));
+    cudaError_t e2 = cudaMalloc(&dw, chunk * 4);
+    if (e2 != cudaSuccess) { cudaFree(dc); CKG(e2); }
+    for (unsigned long long k0 = 0; k0 < m; k0 += chunk) {
+      const unsigned long long c = std::min(chunk, m - k0);
+      cudaError_t e = cudaMemcpyAsync(dc, col + k0, c * 4, cudaMemcpyHostToDevice, g->stream);
+      if (e == cudaSuccess && weight_kind != MLMQ_W_UNIT)
+        e = cudaMemcpyAsync(dw, (const uint32_t*)w + k0, c * 4, cudaMemcpyHostToDevice, g->stream);
+      if (e == cudaSuccess) {
+        interleave_kernel<<<1024, 256, 0, g->stream>>>(dc, dw, g->d_adj + k0, c, weight_kind == MLMQ_W_UNIT);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+      if (e != cudaSuccess) { cudaFree(dc); cudaFree(dw); CKG(e); }
+    }
+    cudaFree(dc);
+    cudaFree(dw);
+  }
+  CKG(cudaStreamSynchronize(g->stream));
+#undef CKG
+  *out = g;
+  return MLMQ_OK;
+}
+
+void mlmq_graph_destroy(mlmq_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  ws_free(g->ws);
+  cudaFree(g->d_off);
+  cudaFree(g->d_adj);
+  cudaFree(g->d_dist);
+  cudaFree(g->d_dist64);
+  cudaFree(g->d_ctl);
+  cudaFree(g->d_audit);
+  cudaFree(g->d_metrics);
+  cudaFree(g->d_scratch);
+  if (g->h_abort) cudaFreeHost(g->h_abort);
+  if (g->ev0) cudaEventDestroy(g->ev0);
+  if (g->ev1) cudaEventDestroy(g->ev1);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  cudaGetLastError();
+  delete g;
+}
+
+int mlmq_graph_device_bytes(const mlmq_graph* g, uint64_t* out) {
+  if (!g || !out) return MLMQ_EINVAL;
+  *out = (g->n + 1) * 8 + g->m * 8 + g->n * 8 + g->ws.bytes;
+  return MLMQ_OK;
+}
+
+int mlmq_auto_groups(const mlmq_graph* gc, const mlmq_config_t* c, int32_t* out) {
+  if (!gc || !c || !out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  mlmq_graph* g = const_cast<mlmq_graph*>(gc);
+  CK(cudaSetDevice(g->device));
+  int st = validate(c);
+  if (st) return st;
+  LaunchShape sh;
+  const int dk = g->wkind == MLMQ_W_F32 ? DK_F32 : (c->dist_mode == MLMQ_DIST_U64 ? DK_U64 : DK_U32);
+  if ((st = launch_shape(g, c, dk, &sh))) return st;
+  *out = sh.max_groups;
+  return MLMQ_OK;
+}
+
+int mlmq_sssp(mlmq_graph* g, uint64_t source, const mlmq_config_t* cfg, uint64_t* dist_out,
+              mlmq_metrics_t* metrics_out, uint64_t* group_metrics, uint64_t group_metrics_cap) {
+  if (!dist_out) { set_last_error("null dist_out"); return MLMQ_EINVAL; }
+  return solve(g, source, cfg, dist_out, false, metrics_out, group_metrics, group_metrics_cap);
+}
+
+int mlmq_sssp_f32(mlmq_graph* g, uint64_t source, const mlmq_config_t* cfg, float* dist_out,
+                  mlmq_metrics_t* metrics_out, uint64_t* group_metrics, uint64_t group_metrics_cap) {
+  if (!dist_out) { set_last_error("null dist_out"); return MLMQ_EINVAL; }
+  return solve(g, source, cfg, dist_out, true, metrics_out, group_metrics, group_metrics_cap);
+}
+
+int mlmq_sssp_device(mlmq_graph* g, uint64_t source, const mlmq_config_t* cfg, mlmq_metrics_t* metrics_out) {
+  return solve(g, source, cfg, nullptr, g && g->wkind == MLMQ_W_F32, metrics_out, nullptr, 0);
+}
+
+int mlmq_last_dist(mlmq_graph* g, uint64_t* dist_out) {
+  if (!g || !dist_out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  std::lock_guard<std::mutex> lk(g->mu);
+  CK(cudaSetDevice(g->device));
+  if (g->last_dk == DK_F32) {
+    CK(cudaMemcpy(dist_out, g->d_dist, g->n * 4, cudaMemcpyDeviceToHost));
+    return MLMQ_OK;
+  }
+  return copy_dist_u64(g, dist_out);
+}
+
+int mlmq_reach(mlmq_graph* g, uint64_t* v_reach, uint64_t* e_reach) {
+  if (!g || !v_reach || !e_reach) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  std::lock_guard<std::mutex> lk(g->mu);
+  CK(cudaSetDevice(g->device));
+  if (g->last_dk < 0) { set_last_error("no solve has run on this graph"); return MLMQ_EINVAL; }
+  CK(cudaMemsetAsync(g->d_scratch, 0, 16, g->stream));
+  const int blocks = (int)std::min<unsigned long long>(8ull * g->sm_count, (g->n + 255) / 256 + 1);
+  if (g->last_dk == DK_U64)
+    reach_kernel<unsigned long long><<<blocks, 256, 0, g->stream>>>((const unsigned long long*)g->d_dist, ~0ull, g->d_off, g->n, g->d_scratch);
+  else
+    reach_kernel<uint32_t><<<blocks, 256, 0, g->stream>>>((const uint32_t*)g->d_dist,
+                                                          g->last_dk == DK_F32 ? 0x7f800000u : 0xFFFFFFFFu,
+                                                          g->d_off, g->n, g->d_scratch);
+  CK(cudaGetLastError());
+  unsigned long long h[2];
+  CK(cudaMemcpyAsync(h, g->d_scratch, 16, cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  *v_reach = h[0];
+  *e_reach = h[1];
+  return MLMQ_OK;
+}
+
+int mlmq_feature_sums(mlmq_graph* g, uint64_t out[10]) {
+  if (!g || !out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  std::lock_guard<std::mutex> lk(g->mu);
+  CK(cudaSetDevice(g->device));
+  CK(cudaMemsetAsync(g->d_scratch, 0, 16 * 8, g->stream));
+  const int blocks = 4 * g->sm_count;
+  feature_sums_kernel<<<blocks, 256, 0, g->stream>>>(g->d_off, g->d_adj, g->n, g->m,
+                                                     g->wkind == MLMQ_W_UNIT, g->d_scratch);
+  CK(cudaGetLastError());
+  if (g->wkind == MLMQ_W_F32) {
+    feature_sums_f32_kernel<<<blocks, 256, 0, g->stream>>>(g->d_adj, g->m, (double*)(g->d_scratch + 8),
+                                                           (unsigned int*)(g->d_scratch + 10));
+    CK(cudaGetLastError());
+  }
+  unsigned long long h[16];
+  CK(cudaMemcpyAsync(h, g->d_scratch, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  out[0] = g->n;
+  out[1] = g->m;
+  out[2] = h[0];
+  out[3] = h[1];
+  out[4] = h[2];
+  out[5] = h[3];
+  if (g->wkind == MLMQ_W_F32) {
+    out[6] = h[8];   // double bits of sum w
+    out[7] = h[9];   // double bits of sum w^2
+    out[8] = 0;
+    out[9] = h[10] & 0xFFFFFFFFull;  // float bits of max w
+  } else {
+    out[6] = h[4];
+    out[7] = h[5];
+    out[8] = h[6];
+    out[9] = h[7];
+  }
+  return MLMQ_OK;
+}
+
+}  // extern "C"
