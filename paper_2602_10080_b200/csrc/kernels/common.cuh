@@ -47,6 +47,15 @@ enum {
   M_RELAX = 0, M_UPD, M_L0E, M_L0D, M_L1E, M_L1D, M_L2E, M_L2D, M_L2A, M_FLUSH, M_SETTLED,
   M_COUNT
 };
+// Debug-only phase profile slots (per warp, clock64 cycles / counts), MLMQ_DEBUG=1.
+enum {
+  P_L0L1 = 0, P_HUB, P_L2R, P_RELAX, P_L2W, P_IDLE, P_NBATCH, P_BATCHSUM, P_NL2R, P_NL2W,
+  P_SPINS, P_CASFAIL, P_L2WELEMS, P_TOTAL, P_COUNT
+};
+constexpr int kMetSlots = 32;  // M_COUNT metric slots + P_COUNT profile slots (smem, per warp)
+constexpr int kProfBase = 16;
+// Debug wait-state codes written to wstate[gid] >> 56
+enum { W_NONE = 0, W_RING_WRITE = 1, W_RING_READ = 2, W_HUB_READ = 3, W_HUB_WRITE = 4, W_HEAP = 5 };
 
 template <int K> struct DT;
 
@@ -242,6 +251,8 @@ struct KParams {
   unsigned long long* ctl;
   const volatile uint32_t* host_abort;
   unsigned long long* metrics;  // [G * M_COUNT]
+  unsigned long long* prof;     // debug: [G * P_COUNT] or null
+  unsigned long long* wstate;   // debug: [G] current wait (code << 56 | ticket) or null
   unsigned long long spin_timeout_ns;
   int smem_per_warp;            // bytes
   int batch_cap, out_cap, spill_cap;  // elements

@@ -65,7 +65,7 @@ struct Worker {
     l1b = l1a + p.l1cap;
     const int l1n = (p.l1type == L1K_NEAR_FAR ? 2 : 1) * p.l1cap;
     met = reinterpret_cast<unsigned long long*>(l1a + l1n);
-    if (lane < M_COUNT) met[lane] = 0;
+    met[lane] = 0;  // metric + profile slots (kMetSlots == 32)
     l0n = 0;
     wc = rc = l0size = 0;
     h1 = n1 = h2 = n2 = 0;
@@ -82,6 +82,17 @@ struct Worker {
 
   __device__ __forceinline__ void count(int f, unsigned long long v) {
     if (lane == 0) met[f] += v;
+  }
+  // debug profile (MLMQ_DEBUG=1): cycles per phase, counts
+  __device__ __forceinline__ unsigned long long pclk() const { return p.prof ? clock64() : 0ull; }
+  __device__ __forceinline__ void pacc(int slot, unsigned long long t0) {
+    if (p.prof && lane == 0) met[kProfBase + slot] += clock64() - t0;
+  }
+  __device__ __forceinline__ void pcnt(int slot, unsigned long long v) {
+    if (p.prof && lane == 0) met[kProfBase + slot] += v;
+  }
+  __device__ __forceinline__ void wstate(int code, unsigned long long tk) {
+    if (p.wstate) p.wstate[gid] = ((unsigned long long)code << 56) | (tk & ((1ull << 56) - 1));
   }
   __device__ __forceinline__ bool stopped() const {
     return ld_relaxed(p.ctl + C_STOP) != 0;
@@ -179,9 +190,10 @@ struct Worker {
   }
 
   // ============================================================ L2: block rings
-  __device__ bool wait_seq(int rid, unsigned long long slot, unsigned long long want) {
+  __device__ bool wait_seq(int rid, unsigned long long slot, unsigned long long want, int why) {
     int ok = 1;
     if (lane == 0) {
+      wstate(why, want);
       unsigned long long* s = p.seq + (size_t)rid * (p.bn_mask + 1) + slot;
       unsigned long long t0 = 0;
       int spins = 0, ns = 32;
@@ -199,6 +211,8 @@ struct Worker {
         __nanosleep(ns);
         if (ns < 1024) ns <<= 1;
       }
+      if (p.prof) met[kProfBase + P_SPINS] += spins;
+      wstate(W_NONE, 0);
     }
     return __shfl_sync(FULL, ok, 0) != 0;
   }
@@ -229,7 +243,7 @@ struct Worker {
     count(M_L2A, 1);
     for (unsigned long long s = 0; s < nseg; ++s) {
       const unsigned long long tk = t + s, slot = tk & p.bn_mask;
-      if (!wait_seq(rid, slot, tk)) return;
+      if (!wait_seq(rid, slot, tk, W_RING_WRITE)) return;
       const int c = min(bs, n - (int)s * bs);
       E* d = slot_data(rid, slot);
       for (int i = lane; i < c; i += 32) d[i] = base[(start + (int)s * bs + i) % cap];
@@ -248,7 +262,7 @@ struct Worker {
     count(M_L2A, 1);
     for (unsigned long long s = 0; s < nseg; ++s) {
       const unsigned long long tk = t + s, slot = tk & p.bn_mask;
-      if (!wait_seq(rid, slot, tk)) return;
+      if (!wait_seq(rid, slot, tk, W_RING_WRITE)) return;
       if (mine && rank / bs == (int)s) slot_data(rid, slot)[rank % bs] = x;
       publish(rid, slot, tk, min(bs, c - (int)s * bs));
     }
@@ -267,6 +281,7 @@ struct Worker {
       while (r < w) {
         unsigned long long old = atomicCAS(rpp, r, r + 1);
         if (old == r) { got = 1; break; }
+        if (p.prof) met[kProfBase + P_CASFAIL] += 1;
         r = old;
         if (r >= w) w = ld_relaxed(wpp);
       }
@@ -275,8 +290,9 @@ struct Worker {
     if (!got) return 0;
     r = __shfl_sync(FULL, r, 0);
     count(M_L2A, 1);
+    pcnt(P_NL2R, 1);
     const unsigned long long slot = r & p.bn_mask;
-    if (!wait_seq(rid, slot, r + 1)) return 0;
+    if (!wait_seq(rid, slot, r + 1, W_RING_READ)) return 0;
     __syncwarp();
     const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
     int c = 0;
@@ -416,6 +432,7 @@ struct Worker {
     int ok = 1;
     if (lane == 0) {
       uint32_t* lk = p.hlock + (size_t)h * 32;
+      wstate(W_HEAP, (unsigned long long)h);
       unsigned long long t0 = 0;
       int spins = 0, ns = 32;
       while (atomicCAS(lk, 0u, 1u) != 0u) {
@@ -432,6 +449,7 @@ struct Worker {
         __nanosleep(ns);
         if (ns < 512) ns <<= 1;
       }
+      wstate(W_NONE, 0);
       __threadfence();
     }
     ok = __shfl_sync(FULL, ok, 0);
@@ -593,7 +611,10 @@ struct Worker {
   // (or heap write counter) itself, claimed before the block is published.
   __device__ void write_back(const E* base, int start, int n, int cap) {
     if (n <= 0) return;
+    const unsigned long long t0 = pclk();
     count(M_L2E, (unsigned long long)n);
+    pcnt(P_NL2W, 1);
+    pcnt(P_L2WELEMS, (unsigned long long)n);
     if (L2K == L2K_FIFO) {
       ring_write(0, base, start, n, cap);
     } else if (L2K == L2K_BUCKET) {
@@ -602,6 +623,7 @@ struct Worker {
       heap_write(mcursor, base, start, n, cap);
       if (p.pnum > 1) mcursor = (mcursor + 1) % p.pnum;
     }
+    pacc(P_L2W, t0);
   }
 
   __device__ int l2_read(E* dst) {
@@ -1057,6 +1079,7 @@ struct Worker {
     HubItem it;
     int ok = 1;
     if (lane == 0) {
+      wstate(W_HUB_READ, r + 1);
       while (ld_acquire(p.hub_seq + slot) != r + 1) {
         if (stopped()) { ok = 0; break; }
         __nanosleep(64);
@@ -1070,6 +1093,7 @@ struct Worker {
         it.u = b.z;
         st_release(p.hub_seq + slot, r + p.hub_mask + 1);
       }
+      wstate(W_NONE, 0);
     }
     if (!__shfl_sync(FULL, ok, 0)) return true;
     it.lo = __shfl_sync(FULL, it.lo, 0);
@@ -1161,27 +1185,43 @@ struct Worker {
   // compose.py:30-54. Returns >0 batch size, -1 when a hub item was processed, 0 on a
   // full miss.
   __device__ int read_cascade() {
+    unsigned long long t0 = pclk();
     if (l0size > 0) {
       const int c = l0_read(batch, L);
       count(M_L0D, (unsigned long long)c);
+      pacc(P_L0L1, t0);
       return c;
     }
     const int c1 = l1_read(batch, L);
+    pacc(P_L0L1, t0);
     if (c1 > 0) {
       count(M_L1D, (unsigned long long)c1);
       return c1;
     }
-    if (hub_try()) return -1;
-    return l2_read(batch);
+    t0 = pclk();
+    if (hub_try()) {
+      pacc(P_HUB, t0);
+      return -1;
+    }
+    pacc(P_HUB, t0);
+    t0 = pclk();
+    const int c2 = l2_read(batch);
+    pacc(P_L2R, t0);
+    return c2;
   }
 
   __device__ void run() {
     int backoff = 0;
+    const unsigned long long tstart = pclk();
     for (;;) {
       if (stopped()) break;
       const int c = read_cascade();
       if (c > 0) {
+        const unsigned long long t0 = pclk();
+        pcnt(P_NBATCH, 1);
+        pcnt(P_BATCHSUM, (unsigned long long)c);
         relax_batch(c);
+        pacc(P_RELAX, t0);
         backoff = 0;
         continue;
       }
@@ -1200,14 +1240,19 @@ struct Worker {
         local_done = 0;
         __syncwarp();
       }
+      const unsigned long long t0 = pclk();
       __nanosleep(32u << min(backoff, 5));
       ++backoff;
+      pacc(P_IDLE, t0);
     }
+    pacc(P_TOTAL, tstart);
     // exit: metric shard + audit evidence
     if (__any_sync(FULL, dist_ovf) && lane == 0) atomicOr(p.ctl + C_DIST_OVF, 1ull);
     const int l1size = n1 + n2;
     if (lane == 0) {
       for (int f = 0; f < M_COUNT; ++f) p.metrics[(size_t)gid * M_COUNT + f] = met[f];
+      if (p.prof)
+        for (int f = 0; f < P_COUNT; ++f) p.prof[(size_t)gid * P_COUNT + f] = met[kProfBase + f];
       if (l0size + l1size + outn) atomicAdd(p.ctl + C_LOCAL_NONEMPTY, (unsigned long long)(l0size + l1size + outn));
     }
   }

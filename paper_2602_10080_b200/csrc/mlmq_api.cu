@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -114,6 +115,9 @@ struct mlmq_graph {
   unsigned long long* d_metrics = nullptr;
   unsigned long long metrics_cap = 0;
   unsigned long long* d_scratch = nullptr;  // 16 words for features / reach
+  unsigned long long* d_prof = nullptr;     // MLMQ_DEBUG: per-warp phase profile
+  unsigned long long* d_wstate = nullptr;   // MLMQ_DEBUG: per-warp wait state
+  unsigned long long prof_cap = 0;
   uint32_t* h_abort = nullptr;
   uint32_t* d_abort = nullptr;
   Workspace ws;
@@ -174,7 +178,7 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
   s->batch_cap = std::max(c->block_size, 32);
   s->spill_cap = L * c->l0_capacity + L;
   const int l1n = (c->l1_type == MLMQ_L1_NEAR_FAR ? 2 : 1) * c->l1_capacity;
-  long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n) + M_COUNT * 8;
+  long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n) + kMetSlots * 8;
   bytes = (bytes + 15) / 16 * 16;
   int max_smem_block = 0;
   CK(cudaDeviceGetAttribute(&max_smem_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
@@ -286,6 +290,51 @@ double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+bool debug_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MLMQ_DEBUG");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// MLMQ_DEBUG=1: per-phase cycle breakdown and the wait states of stuck warps.
+void debug_dump(mlmq_graph* g, int G, const char* tag) {
+  std::vector<unsigned long long> pr((size_t)G * P_COUNT), ws((size_t)G);
+  if (cudaMemcpy(pr.data(), g->d_prof, pr.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(ws.data(), g->d_wstate, ws.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    fprintf(stderr, "[mlmq debug] copy failed\n");
+    return;
+  }
+  unsigned long long tot[P_COUNT] = {0};
+  for (int i = 0; i < G; ++i)
+    for (int f = 0; f < P_COUNT; ++f) tot[f] += pr[(size_t)i * P_COUNT + f];
+  const double T = tot[P_TOTAL] ? (double)tot[P_TOTAL] : 1.0;
+  fprintf(stderr,
+          "[mlmq debug] %s G=%d cycles/warp=%.3g  L0L1 %.1f%%  hub %.1f%%  L2read %.1f%%  relax %.1f%% "
+          "(of which L2write %.1f%%)  idle %.1f%% | batches %llu avg %.1f  L2 reads %llu  L2 writes %llu "
+          "(%.1f elems avg)  spins %llu  casfail %llu\n",
+          tag, G, T / G, 100 * tot[P_L0L1] / T, 100 * tot[P_HUB] / T, 100 * tot[P_L2R] / T,
+          100 * tot[P_RELAX] / T, 100 * tot[P_L2W] / T, 100 * tot[P_IDLE] / T, tot[P_NBATCH],
+          tot[P_NBATCH] ? (double)tot[P_BATCHSUM] / tot[P_NBATCH] : 0.0, tot[P_NL2R], tot[P_NL2W],
+          tot[P_NL2W] ? (double)tot[P_L2WELEMS] / tot[P_NL2W] : 0.0, tot[P_SPINS], tot[P_CASFAIL]);
+  int hist[8] = {0};
+  int shown = 0;
+  for (int i = 0; i < G; ++i) {
+    const int code = (int)(ws[i] >> 56);
+    hist[code & 7]++;
+    if (code && shown < 16) {
+      fprintf(stderr, "[mlmq debug]   warp %d waits code %d ticket %llu\n", i, code,
+              ws[i] & ((1ull << 56) - 1));
+      ++shown;
+    }
+  }
+  fprintf(stderr, "[mlmq debug]   wait states: none %d ringW %d ringR %d hubR %d hubW %d heap %d\n",
+          hist[0], hist[1], hist[2], hist[3], hist[4], hist[5]);
+}
+
 // One attempt at a given distance kind.  Returns MLMQ_OK, an error, or 100 when the
 // optimistic u32 distances overflowed (caller re-runs in u64).
 int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, int dk,
@@ -308,6 +357,18 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     g->metrics_cap = G;
   }
   Workspace& w = g->ws;
+  const bool dbg = debug_enabled();
+  if (dbg && g->prof_cap < (unsigned long long)G) {
+    cudaFree(g->d_prof);
+    cudaFree(g->d_wstate);
+    CK(cudaMalloc(&g->d_prof, (size_t)G * P_COUNT * 8));
+    CK(cudaMalloc(&g->d_wstate, (size_t)G * 8));
+    g->prof_cap = G;
+  }
+  if (dbg) {
+    CK(cudaMemset(g->d_prof, 0, (size_t)G * P_COUNT * 8));
+    CK(cudaMemset(g->d_wstate, 0, (size_t)G * 8));
+  }
   KParams p;
   std::memset(&p, 0, sizeof(p));
   p.off = g->d_off;
@@ -329,7 +390,8 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.nb = std::min(c->node_batch, 32);
   p.G = G;
   if (dk == DK_F32) {
-    float nf = (float)c->delta_nf, ff = (float)c->filter_f;
+    // a zero NF step would leave far elements stranded in L1: clamp to the smallest step
+    float nf = c->delta_nf > 0 ? (float)c->delta_nf : 1e-30f, ff = (float)c->filter_f;
     uint32_t bnf, bff;
     std::memcpy(&bnf, &nf, 4);
     std::memcpy(&bff, &ff, 4);
@@ -339,7 +401,7 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     p.delta_i = 1;
   } else {
     const double cap = dk == DK_U32 ? 4294967294.0 : 1.8e19;
-    p.delta_nf_s = (unsigned long long)std::min(std::max(c->delta_nf, 0.0), cap);
+    p.delta_nf_s = (unsigned long long)std::min(std::max(c->delta_nf, 1.0), cap);
     p.filter_f_s = (unsigned long long)std::min(std::max(c->filter_f, 0.0), cap);
     p.delta_i = (unsigned long long)std::max(1.0, c->delta);
     p.delta_f = (double)p.delta_i;
@@ -365,6 +427,8 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.ctl = g->d_ctl;
   p.host_abort = g->d_abort;
   p.metrics = g->d_metrics;
+  p.prof = dbg ? g->d_prof : nullptr;
+  p.wstate = dbg ? g->d_wstate : nullptr;
   const double spin = c->spin_timeout_s > 0 ? c->spin_timeout_s : 15.0;
   p.spin_timeout_ns = (unsigned long long)(spin * 1e9);
   p.smem_per_warp = sh.smem_per_warp;
@@ -406,6 +470,7 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
         abort_t = t;
       }
       if (aborted && t - abort_t > 5.0) {
+        if (dbg) debug_dump(g, G, "stuck-after-abort");
         w.dirty = true;
         set_last_error("worker failed to stop after abort");
         return MLMQ_EENGINE;
@@ -417,6 +482,12 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   }
   unsigned long long au[kAuditWords];
   CK(cudaMemcpy(au, g->d_audit, sizeof(au), cudaMemcpyDeviceToHost));
+  if (dbg) {
+    char tag[160];
+    snprintf(tag, sizeof(tag), "l1=%d l2=%d dk=%d err=%llu done=%llu reserve=%llu epoch=%llu", c->l1_type,
+             c->l2_type, dk, au[6], au[0], au[1], au[13]);
+    debug_dump(g, G, tag);
+  }
   const unsigned long long err = au[6];
   if (err == ERR_ABORT) {
     w.dirty = true;
@@ -682,6 +753,8 @@ void mlmq_graph_destroy(mlmq_graph* g) {
   cudaFree(g->d_audit);
   cudaFree(g->d_metrics);
   cudaFree(g->d_scratch);
+  cudaFree(g->d_prof);
+  cudaFree(g->d_wstate);
   if (g->h_abort) cudaFreeHost(g->h_abort);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
