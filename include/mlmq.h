@@ -80,7 +80,9 @@ typedef struct {
   double watchdog_s;                /* engine.py:267-279; <= 0 disables               */
   double spin_timeout_s;            /* ring-slot wait before QueueOverflowError (l2.py:94) */
   int32_t hub_chunk;                /* edges per hub work item (0 = library default)  */
-  int32_t reserved[7];
+  int32_t share;                    /* 1: eager L1/L0 write-back while groups are idle */
+  int32_t fifo_park;                /* 1: FIFO readers take unconditional tickets      */
+  int32_t reserved[5];
 } mlmq_config_t;
 
 /*

@@ -41,7 +41,8 @@ class Config(ctypes.Structure):
         ("th_v", ctypes.c_int32), ("dup_elim", ctypes.c_int32),
         ("unit_weights", ctypes.c_int32), ("dist_mode", ctypes.c_int32),
         ("watchdog_s", ctypes.c_double), ("spin_timeout_s", ctypes.c_double),
-        ("hub_chunk", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7),
+        ("hub_chunk", ctypes.c_int32), ("share", ctypes.c_int32), ("fifo_park", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 5),
     ]
 
 

@@ -45,6 +45,7 @@ __global__ void init_kernel(S* dist, unsigned long long n, unsigned long long so
   ctl[C_DIST_OVF] = 0;
   ctl[C_LOCAL_NONEMPTY] = 0;
   ctl[C_HUB_ITEMS] = 0;
+  ctl[C_IDLE] = 0;
   for (int i = 0; i < 4; ++i) ctl[C_DIAG + i] = 0;
   unsigned long long reserve = ctl[C_HUB_WP];
   for (int r = 0; r < p.nrings; ++r) reserve += p.ptrs[(size_t)r * 32];
@@ -75,14 +76,16 @@ __global__ void init_kernel(S* dist, unsigned long long n, unsigned long long so
 
 // K5 (_Run.audit engine.py:229-242): reserve == done, rings drained, heaps empty,
 // no group holding elements.
-__global__ void audit_kernel(KParams p, unsigned long long* out) {
+// With parked FIFO readers (fifo_fix), tickets still pending at termination are
+// retired here: their slots are marked consumed and the write pointer catches up.
+__global__ void audit_kernel(KParams p, unsigned long long* out, int fifo_fix) {
   __shared__ unsigned long long s_res[256], s_bad[256], s_hs[256];
   const int t = threadIdx.x;
   unsigned long long res = 0, bad = 0, hs = 0;
   for (int r = t; r < p.nrings; r += blockDim.x) {
     const unsigned long long w = p.ptrs[(size_t)r * 32], rd = p.ptrs[(size_t)r * 32 + 16];
     res += w;
-    bad += (w != rd);
+    bad += fifo_fix ? (rd < w) : (w != rd);
   }
   for (int h = t; h < p.pnum; h += blockDim.x) {
     res += p.hwc[(size_t)h * 16];
@@ -113,6 +116,12 @@ __global__ void audit_kernel(KParams p, unsigned long long* out) {
     for (int i = 0; i < 4; ++i) out[8 + i] = ctl[C_DIAG + i];
     out[12] = ctl[C_HUB_ITEMS];
     out[13] = ctl[C_EPOCH];
+    if (fifo_fix) {
+      const unsigned long long w = p.ptrs[0], rd = p.ptrs[16];
+      for (unsigned long long tk = w; tk < rd; ++tk) p.seq[tk & p.bn_mask] = tk + p.bn_mask + 1;
+      if (rd > w) p.ptrs[0] = rd;
+      __threadfence();
+    }
   }
 }
 

@@ -39,7 +39,8 @@ enum : int {
   C_LOCAL_NONEMPTY = 112, // audit: sum of L0+L1 sizes at exit (engine.py:233-237)
   C_DIAG = 128,           // overflow diagnostics: ring, slot, write_ptr, read_ptr
   C_HUB_ITEMS = 144,      // hub items pushed
-  C_WORDS = 160
+  C_IDLE = 160,           // number of groups currently idle (demand signal for eager spill)
+  C_WORDS = 176
 };
 
 // Per-group metric slots, in METRIC_FIELDS order (core.py:142-154).
@@ -255,6 +256,9 @@ struct KParams {
   unsigned long long* wstate;   // debug: [G] current wait (code << 56 | ticket) or null
   unsigned long long spin_timeout_ns;
   int smem_per_warp;            // bytes
+  int share;                    // eager spill to L2 when groups are idle (B200 extension)
+  int fifo_park;                // FIFO readers take unconditional tickets
+  int bscratch;                 // bucket writes use the per-warp histogram scratch (bmax <= 256)
   int batch_cap, out_cap, spill_cap;  // elements
 };
 

@@ -35,6 +35,9 @@ struct Worker {
   E* l1a;
   E* l1b;
   unsigned long long* met;
+  unsigned long long* btick;  // bucket write scratch (smem): ticket base per bucket
+  uint32_t* bhist;            // elements per bucket
+  uint32_t* bcur;             // scatter cursor per bucket
   int lane, gid, L;
 
   // L0: per-lane register FIFO (shift register, pop at index 0)
@@ -53,6 +56,7 @@ struct Worker {
   int mcursor;
   int outn;
   bool dist_ovf;
+  bool idle;
 
   __device__ Worker(const KParams& prm, unsigned char* sm, int g, int ln) : p(prm), lane(ln), gid(g) {
     L = p.L;
@@ -66,6 +70,9 @@ struct Worker {
     const int l1n = (p.l1type == L1K_NEAR_FAR ? 2 : 1) * p.l1cap;
     met = reinterpret_cast<unsigned long long*>(l1a + l1n);
     met[lane] = 0;  // metric + profile slots (kMetSlots == 32)
+    btick = met + kMetSlots;
+    bhist = reinterpret_cast<uint32_t*>(btick + (p.bscratch ? p.bmax : 0));
+    bcur = bhist + (p.bscratch ? p.bmax : 0);
     l0n = 0;
     wc = rc = l0size = 0;
     h1 = n1 = h2 = n2 = 0;
@@ -77,6 +84,8 @@ struct Worker {
     mcursor = p.pnum > 0 ? gid % p.pnum : 0;
     outn = 0;
     dist_ovf = false;
+    pend = ~0ull;
+    idle = false;
     __syncwarp();
   }
 
@@ -190,86 +199,116 @@ struct Worker {
   }
 
   // ============================================================ L2: block rings
-  __device__ bool wait_seq(int rid, unsigned long long slot, unsigned long long want, int why) {
-    int ok = 1;
-    if (lane == 0) {
-      wstate(why, want);
-      unsigned long long* s = p.seq + (size_t)rid * (p.bn_mask + 1) + slot;
-      unsigned long long t0 = 0;
-      int spins = 0, ns = 32;
-      while (ld_acquire(s) != want) {
-        if (++spins % 64 == 0) {
-          if (stopped()) { ok = 0; break; }
-          unsigned long long now = globaltimer_ns();
-          if (t0 == 0) t0 = now;
-          else if (now - t0 > p.spin_timeout_ns) {
-            raise_error(ERR_OVERFLOW, (unsigned long long)rid, slot, ld_relaxed(wp(rid)), ld_relaxed(rp(rid)));
-            ok = 0;
-            break;
-          }
-        }
-        __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
-      }
-      if (p.prof) met[kProfBase + P_SPINS] += spins;
-      wstate(W_NONE, 0);
-    }
-    return __shfl_sync(FULL, ok, 0) != 0;
+  // Per-slot sequence numbers (Vyukov): slot s is free for ticket t when seq == t,
+  // holds ticket t's block when seq == t + 1, and is freed by the reader to t + bn.
+  // Unlike the reference's bare tags (l2.py:110-114) this is ABA-safe on wrap-around.
+  __device__ __forceinline__ unsigned long long* seq_ptr(int rid, unsigned long long slot) const {
+    return p.seq + (size_t)rid * (p.bn_mask + 1) + slot;
   }
-
   __device__ __forceinline__ E* slot_data(int rid, unsigned long long slot) const {
     return reinterpret_cast<E*>(p.data) + ((size_t)rid * (p.bn_mask + 1) + slot) * p.bs;
   }
 
-  __device__ __forceinline__ void publish(int rid, unsigned long long slot, unsigned long long tk, int c) {
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) {
-      const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
-      p.cnt[i] = (uint32_t)c;
-      st_release(p.seq + i, tk + 1);
+  // Per-lane bounded spin until *s == want; false on stop or timeout (overflow error).
+  __device__ bool lane_spin(const unsigned long long* s, unsigned long long want, int rid,
+                            unsigned long long slot) {
+    unsigned long long t0 = 0;
+    int spins = 0, ns = 32;
+    while (ld_acquire(s) != want) {
+      if (++spins % 64 == 0) {
+        if (stopped()) return false;
+        const unsigned long long now = globaltimer_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > p.spin_timeout_ns) {
+          raise_error(ERR_OVERFLOW, (unsigned long long)rid, slot, ld_relaxed(wp(rid)), ld_relaxed(rp(rid)));
+          return false;
+        }
+      }
+      __nanosleep(ns);
+      if (ns < 1024) ns <<= 1;
     }
+    if (p.prof) atomicAdd(met + kProfBase + P_SPINS, (unsigned long long)spins);
+    return true;
   }
 
-  // Writer (l2.py:96-114): one fetch-add claims ceil(n/bs) tickets, each segment waits
-  // for its slot's sequence number (ABA-safe, unlike bare tags) and is published whole.
+  // Wait (lanes in parallel) until the nseg slots of tickets t..t+nseg-1 are free.
+  __device__ bool wait_free(int rid, unsigned long long t, int nseg) {
+    bool ok = true;
+    if (lane == 0) wstate(W_RING_WRITE, t);
+    for (int sg = lane; sg < nseg; sg += 32) {
+      const unsigned long long tk = t + sg, slot = tk & p.bn_mask;
+      if (ok && !lane_spin(seq_ptr(rid, slot), tk, rid, slot)) ok = false;
+    }
+    ok = __all_sync(FULL, ok);
+    if (lane == 0) wstate(W_NONE, 0);
+    return ok;
+  }
+
+  // Publish (lanes in parallel) the nseg blocks of tickets t.. holding `n` elements.
+  __device__ void publish_all(int rid, unsigned long long t, int nseg, int n) {
+    __threadfence();
+    __syncwarp();
+    for (int sg = lane; sg < nseg; sg += 32) {
+      const unsigned long long tk = t + sg, slot = tk & p.bn_mask;
+      const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
+      p.cnt[i] = (uint32_t)min(p.bs, n - sg * p.bs);
+      st_release(p.seq + i, tk + 1);
+    }
+    __syncwarp();
+  }
+
+  // Writer (l2.py:96-114): one fetch-add claims ceil(n/bs) tickets; all slot waits,
+  // element stores and publications of the write proceed warp-parallel.
   __device__ void ring_write(int rid, const E* base, int start, int n, int cap) {
     if (n <= 0) return;
     const int bs = p.bs;
-    const unsigned long long nseg = (unsigned long long)((n + bs - 1) / bs);
+    const int nseg = (n + bs - 1) / bs;
     unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(wp(rid), nseg);
+    if (lane == 0) t = atomicAdd(wp(rid), (unsigned long long)nseg);
     t = __shfl_sync(FULL, t, 0);
     count(M_L2A, 1);
-    for (unsigned long long s = 0; s < nseg; ++s) {
-      const unsigned long long tk = t + s, slot = tk & p.bn_mask;
-      if (!wait_seq(rid, slot, tk, W_RING_WRITE)) return;
-      const int c = min(bs, n - (int)s * bs);
-      E* d = slot_data(rid, slot);
-      for (int i = lane; i < c; i += 32) d[i] = base[(start + (int)s * bs + i) % cap];
-      publish(rid, slot, tk, c);
+    if (!wait_free(rid, t, nseg)) return;
+    for (int i = lane; i < n; i += 32) {
+      const int sg = i / bs;
+      slot_data(rid, (t + sg) & p.bn_mask)[i - sg * bs] = base[(start + i) % cap];
     }
+    publish_all(rid, t, nseg, n);
   }
 
   // Same, with the elements held one per lane (grp = writing lanes, rank within grp).
   __device__ void ring_write_lanes(int rid, unsigned grp, int rank, const E& x, bool mine) {
     const int c = __popc(grp);
     const int bs = p.bs;
-    const unsigned long long nseg = (unsigned long long)((c + bs - 1) / bs);
+    const int nseg = (c + bs - 1) / bs;
     unsigned long long t = 0;
-    if (lane == 0) t = atomicAdd(wp(rid), nseg);
+    if (lane == 0) t = atomicAdd(wp(rid), (unsigned long long)nseg);
     t = __shfl_sync(FULL, t, 0);
     count(M_L2A, 1);
-    for (unsigned long long s = 0; s < nseg; ++s) {
-      const unsigned long long tk = t + s, slot = tk & p.bn_mask;
-      if (!wait_seq(rid, slot, tk, W_RING_WRITE)) return;
-      if (mine && rank / bs == (int)s) slot_data(rid, slot)[rank % bs] = x;
-      publish(rid, slot, tk, min(bs, c - (int)s * bs));
+    if (!wait_free(rid, t, nseg)) return;
+    if (mine) {
+      const int sg = rank / bs;
+      slot_data(rid, (t + sg) & p.bn_mask)[rank - sg * bs] = x;
     }
+    publish_all(rid, t, nseg, c);
   }
 
-  // Reader (l2.py:137-162): claim a ticket only when a written block exists, then wait
-  // for the in-flight writer (never leaves a dangling claim), copy, free the slot.
+  // Copy ticket r's published block out and free the slot.
+  __device__ int take_block(int rid, unsigned long long r, E* dst) {
+    const unsigned long long slot = r & p.bn_mask;
+    const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
+    int c = 0;
+    if (lane == 0) c = (int)__ldcg(p.cnt + i);
+    c = __shfl_sync(FULL, c, 0);
+    const E* d = slot_data(rid, slot);
+    for (int k = lane; k < c; k += 32) dst[k] = ld_cg_elem(d + k);
+    __syncwarp();
+    if (lane == 0) st_release(p.seq + i, r + p.bn_mask + 1);
+    pcnt(P_NL2R, 1);
+    return c;
+  }
+
+  // Conditional reader (l2.py:137-162): claim a ticket only when a written block
+  // exists, then wait for the in-flight writer; never leaves a dangling claim.
   __device__ int ring_read(int rid, E* dst) {
     unsigned long long r = 0;
     int got = 0;
@@ -290,18 +329,36 @@ struct Worker {
     if (!got) return 0;
     r = __shfl_sync(FULL, r, 0);
     count(M_L2A, 1);
-    pcnt(P_NL2R, 1);
     const unsigned long long slot = r & p.bn_mask;
-    if (!wait_seq(rid, slot, r + 1, W_RING_READ)) return 0;
+    bool ok = true;
+    if (lane == 0) {
+      wstate(W_RING_READ, r + 1);
+      ok = lane_spin(seq_ptr(rid, slot), r + 1, rid, slot);
+      wstate(W_NONE, 0);
+    }
+    if (!__shfl_sync(FULL, (int)ok, 0)) return 0;
     __syncwarp();
-    const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
-    int c = 0;
-    if (lane == 0) c = (int)__ldcg(p.cnt + i);
-    c = __shfl_sync(FULL, c, 0);
-    const E* d = slot_data(rid, slot);
-    for (int k = lane; k < c; k += 32) dst[k] = ld_cg_elem(d + k);
+    return take_block(rid, r, dst);
+  }
+
+  // Parked FIFO reader: one unconditional fetch-add takes the next
+  // ticket; the ticket persists in a register ("pending", l2.py:151-154) and the warp
+  // polls only its own slot, so idle warps do not contend on the read pointer.
+  // Tickets still pending at termination are retired by the audit kernel.
+  unsigned long long pend;
+  __device__ int fifo_read(E* dst) {
+    if (pend == ~0ull) {
+      unsigned long long r = 0;
+      if (lane == 0) r = atomicAdd(rp(0), 1ull);
+      pend = __shfl_sync(FULL, r, 0);
+      count(M_L2A, 1);
+    }
+    int ready = 0;
+    if (lane == 0) ready = ld_acquire(seq_ptr(0, pend & p.bn_mask)) == pend + 1;
+    if (!__shfl_sync(FULL, ready, 0)) return 0;
     __syncwarp();
-    if (lane == 0) st_release(p.seq + i, r + p.bn_mask + 1);
+    const int c = take_block(0, pend, dst);
+    pend = ~0ull;
     return c;
   }
 
@@ -337,18 +394,74 @@ struct Worker {
   }
 
   // l2.py:209-233: rel = 0 below the floor, (d-base)//Δ above, clamped to bmax-1.
+  // Warp-parallel: (1) per-bucket histogram in shared memory, (2) one ticket fetch-add
+  // per non-empty bucket, (3) parallel slot waits, (4) scatter, (5) parallel publish.
   __device__ void bucket_write(const E* base, int start, int n, int cap) {
     const unsigned long long e = ld_relaxed(p.ctl + C_EPOCH);
-    for (int o = 0; o < n; o += 32) {
-      const bool has = o + lane < n;
-      E x;
-      int f = 0;
-      if (has) {
-        x = base[(start + o + lane) % cap];
-        f = (int)((e + (unsigned long long)bucket_rel(x.d, e)) % (unsigned long long)p.bmax);
+    const unsigned long long bm = (unsigned long long)p.bmax;
+    if (!p.bscratch) {  // very wide windows: per-round grouping
+      for (int o = 0; o < n; o += 32) {
+        const bool has = o + lane < n;
+        E x;
+        int f = 0;
+        if (has) {
+          x = base[(start + o + lane) % cap];
+          f = (int)((e + (unsigned long long)bucket_rel(x.d, e)) % bm);
+        }
+        bucket_scatter_lanes(has, x, f);
       }
-      bucket_scatter_lanes(has, x, f);
+      return;
     }
+    const int bs = p.bs;
+    for (int b = lane; b < p.bmax; b += 32) { bhist[b] = 0; bcur[b] = 0; }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const E x = base[(start + i) % cap];
+      atomicAdd(bhist + (int)((e + (unsigned long long)bucket_rel(x.d, e)) % bm), 1u);
+    }
+    __syncwarp();
+    int used = 0;
+    for (int b = lane; b < p.bmax; b += 32) {
+      const int c = (int)bhist[b];
+      if (c) {
+        btick[b] = atomicAdd(wp(b), (unsigned long long)((c + bs - 1) / bs));
+        ++used;
+      }
+    }
+    count(M_L2A, (unsigned long long)__reduce_add_sync(FULL, used));
+    __syncwarp();
+    bool ok = true;
+    if (lane == 0) wstate(W_RING_WRITE, e);
+    for (int b = lane; b < p.bmax; b += 32) {
+      const int c = (int)bhist[b];
+      const int nseg = (c + bs - 1) / bs;
+      for (int sg = 0; ok && sg < nseg; ++sg) {
+        const unsigned long long tk = btick[b] + sg, slot = tk & p.bn_mask;
+        ok = lane_spin(seq_ptr(b, slot), tk, b, slot);
+      }
+    }
+    if (lane == 0) wstate(W_NONE, 0);
+    if (!__all_sync(FULL, ok)) return;
+    for (int i = lane; i < n; i += 32) {
+      const E x = base[(start + i) % cap];
+      const int f = (int)((e + (unsigned long long)bucket_rel(x.d, e)) % bm);
+      const int r = (int)atomicAdd(bcur + f, 1u);
+      const int sg = r / bs;
+      slot_data(f, (btick[f] + sg) & p.bn_mask)[r - sg * bs] = x;
+    }
+    __threadfence();
+    __syncwarp();
+    for (int b = lane; b < p.bmax; b += 32) {
+      const int c = (int)bhist[b];
+      const int nseg = (c + bs - 1) / bs;
+      for (int sg = 0; sg < nseg; ++sg) {
+        const unsigned long long tk = btick[b] + sg, slot = tk & p.bn_mask;
+        const size_t i = (size_t)b * (p.bn_mask + 1) + slot;
+        p.cnt[i] = (uint32_t)min(bs, c - sg * bs);
+        st_release(p.seq + i, tk + 1);
+      }
+    }
+    __syncwarp();
   }
 
   // l2.py:235-295: scan bnum buckets from the floor; rebin stale-slot elements; advance
@@ -629,7 +742,7 @@ struct Worker {
   __device__ int l2_read(E* dst) {
     int c;
     if (L2K == L2K_FIFO) {
-      c = ring_read(0, dst);
+      c = p.fifo_park ? fifo_read(dst) : ring_read(0, dst);
       if (c > 0) local_done += 1;
     } else if (L2K == L2K_BUCKET) {
       c = bucket_read(dst);
@@ -1181,6 +1294,34 @@ struct Worker {
     flush_out(true);
   }
 
+  // ============================================================ eager sharing
+  // B200 extension of the cache-like collaboration: thousands of warps
+  // starve if a few hoard work in private L0/L1, so while any group is idle a group
+  // holding more than two batches of local work writes its L1 (or, with L1 empty, its
+  // L0) back to L2 where the idle groups can read it.
+  __device__ void maybe_share() {
+    if (!p.share) return;
+    const int local = l0size + n1 + n2;
+    if (local <= 2 * L) return;
+    unsigned long long idle_now = 0;
+    if (lane == 0) idle_now = ld_relaxed(p.ctl + C_IDLE);
+    if (__shfl_sync(FULL, idle_now, 0) == 0) return;
+    const int cap = p.l1cap;
+    if (n1 + n2 > 0) {
+      count(M_L1D, (unsigned long long)(n1 + n2));
+      count(M_FLUSH, 1);
+      write_back(l1a, h1, n1, cap);
+      if (n2) write_back(l1b, h2, n2, cap);
+      h1 = n1 = h2 = n2 = 0;
+      wcount = 0;
+    } else {
+      const int ns = l0_drain(spill);
+      count(M_L0D, (unsigned long long)ns);
+      l0size = 0;
+      write_back(spill, 0, ns, LINEAR);
+    }
+  }
+
   // ============================================================ read cascade
   // compose.py:30-54. Returns >0 batch size, -1 when a hub item was processed, 0 on a
   // full miss.
@@ -1216,19 +1357,29 @@ struct Worker {
     for (;;) {
       if (stopped()) break;
       const int c = read_cascade();
+      if (c != 0 && idle) {
+        idle = false;
+        if (lane == 0) atomicAdd(p.ctl + C_IDLE, ~0ull);  // -1
+      }
       if (c > 0) {
         const unsigned long long t0 = pclk();
         pcnt(P_NBATCH, 1);
         pcnt(P_BATCHSUM, (unsigned long long)c);
         relax_batch(c);
         pacc(P_RELAX, t0);
+        maybe_share();
         backoff = 0;
         continue;
       }
       if (c < 0) {
         flush_out(true);
+        maybe_share();
         backoff = 0;
         continue;
+      }
+      if (!idle) {
+        idle = true;
+        if (lane == 0) atomicAdd(p.ctl + C_IDLE, 1ull);
       }
       // full miss: flush local_done (l2.py:56-62)
       if (local_done) {

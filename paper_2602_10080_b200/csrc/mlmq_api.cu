@@ -166,6 +166,7 @@ struct LaunchShape {
   int smem_per_warp = 0, wpb = 0;
   int batch_cap = 0, spill_cap = 0;
   int max_groups = 0;
+  int bscratch = 0;
 };
 
 int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) {
@@ -178,7 +179,9 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
   s->batch_cap = std::max(c->block_size, 32);
   s->spill_cap = L * c->l0_capacity + L;
   const int l1n = (c->l1_type == MLMQ_L1_NEAR_FAR ? 2 : 1) * c->l1_capacity;
-  long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n) + kMetSlots * 8;
+  s->bscratch = (s->l2k == L2K_BUCKET && c->bmax <= 256) ? 1 : 0;
+  long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n) + kMetSlots * 8 +
+                    (s->bscratch ? 16LL * c->bmax : 0LL);
   bytes = (bytes + 15) / 16 * 16;
   int max_smem_block = 0;
   CK(cudaDeviceGetAttribute(&max_smem_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
@@ -435,6 +438,9 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.batch_cap = sh.batch_cap;
   p.out_cap = kOutCap;
   p.spill_cap = sh.spill_cap;
+  p.share = c->share ? 1 : 0;
+  p.fifo_park = (sh.l2k == L2K_FIFO && c->fifo_park) ? 1 : 0;
+  p.bscratch = sh.bscratch;
 
   *g->h_abort = 0;
   const int blocks = (G + 1 + sh.wpb - 1) / sh.wpb;
@@ -449,7 +455,7 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   void* args[] = {(void*)&p};
   CK(cudaLaunchCooperativeKernel(sh.fn, dim3(blocks), dim3(sh.wpb * 32), args,
                                  (size_t)sh.wpb * sh.smem_per_warp, g->stream));
-  audit_kernel<<<1, 256, 0, g->stream>>>(p, g->d_audit);
+  audit_kernel<<<1, 256, 0, g->stream>>>(p, g->d_audit, p.fifo_park);
   CK(cudaGetLastError());
   CK(cudaEventRecord(g->ev1, g->stream));
 

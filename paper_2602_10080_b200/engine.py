@@ -45,6 +45,8 @@ class EngineConfig:
     hub_chunk: int = 0
     spin_timeout_s: float = 15.0
     device: int = 0
+    share: bool = True       # eager write-back to L2 while groups idle (B200 extension)
+    fifo_park: bool = True   # FIFO readers park on unconditional tickets
 
 
 class SsspResult:
@@ -175,6 +177,8 @@ def _native_config(cfg: MlmqConfig, eng: EngineConfig, unit_weights: bool,
     c.watchdog_s = float(watchdog_s or 0)
     c.spin_timeout_s = float(eng.spin_timeout_s)
     c.hub_chunk = int(eng.hub_chunk)
+    c.share = 1 if eng.share else 0
+    c.fifo_park = 1 if eng.fifo_park else 0
     return c
 
 
