@@ -24,7 +24,8 @@ enum {
   ERR_OVERFLOW = 1,      // ring slot stayed busy (l2.py:116-135)
   ERR_ABORT = 2,         // host watchdog abort (engine.py:267-272)
   ERR_HEAP_OVERFLOW = 3, // batch-heap node pool exhausted
-  ERR_HUB_OVERFLOW = 4   // hub work ring slot stayed busy
+  ERR_HUB_OVERFLOW = 4,  // hub work ring slot stayed busy
+  ERR_CORRUPT = 5        // a queue element named a vertex >= n (internal error)
 };
 
 // Control block: u64 words, every hot word on its own 128-byte line.

@@ -57,6 +57,7 @@ struct Worker {
   int outn;
   bool dist_ovf;
   bool idle;
+  int last_src;  // level that served the current batch (1 L0, 2 L1, 3 L2) for diagnostics
 
   __device__ Worker(const KParams& prm, unsigned char* sm, int g, int ln) : p(prm), lane(ln), gid(g) {
     L = p.L;
@@ -299,6 +300,10 @@ struct Worker {
     int c = 0;
     if (lane == 0) c = (int)__ldcg(p.cnt + i);
     c = __shfl_sync(FULL, c, 0);
+    if (c < 0 || c > p.bs) {
+      if (lane == 0) raise_error(ERR_CORRUPT, 10ull + rid, (unsigned long long)c, (unsigned long long)gid, r);
+      return 0;
+    }
     const E* d = slot_data(rid, slot);
     for (int k = lane; k < c; k += 32) dst[k] = ld_cg_elem(d + k);
     __syncwarp();
@@ -1038,6 +1043,10 @@ struct Worker {
       return;
     }
     const int before = l0size;
+    if (k > L || l0size > L * p.l0cap) {
+      if (lane == 0) raise_error(ERR_CORRUPT, 30, (unsigned long long)k, (unsigned long long)gid, (unsigned long long)l0size);
+      return;
+    }
     int ns = l0_drain(spill);
     if (has && lane >= f) spill[ns + lane - f] = b;
     ns += k - f;
@@ -1093,6 +1102,10 @@ struct Worker {
     for (int j = 0; j < U; ++j)
       if (act[j]) act[j] = nd[j] < atomicMin(dist + v[j], nd[j]);
     const int tot = __reduce_add_sync(FULL, c);
+    if (outn < 0 || outn >= L) {
+      if (lane == 0) raise_error(ERR_CORRUPT, 20, (unsigned long long)outn, (unsigned long long)gid, 0);
+      outn = 0;
+    }
     int upd = 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
@@ -1224,6 +1237,10 @@ struct Worker {
 
   // engine.py:171-227 for one batch in shared memory
   __device__ void relax_batch(int nb) {
+    if (nb > p.batch_cap) {
+      if (lane == 0) raise_error(ERR_CORRUPT, 40, (unsigned long long)nb, (unsigned long long)gid, 0);
+      return;
+    }
     for (int base = 0; base < nb; base += 32) {
       const int i = base + lane;
       bool valid = i < nb;
@@ -1232,6 +1249,13 @@ struct Worker {
       unsigned long long lo = 0, hi = 0;
       if (valid) {
         e = batch[i];
+        if (e.v >= p.n) {  // never expected: report instead of faulting
+          raise_error(ERR_CORRUPT, (unsigned long long)last_src, (unsigned long long)e.v,
+                      (unsigned long long)gid, (unsigned long long)i | ((unsigned long long)nb << 32));
+          valid = false;
+        }
+      }
+      if (valid) {
         const S cur = ldcg_dist(dist + e.v);
         if (p.dup && e.d > cur) valid = false;  // stale duplicate (engine.py:190-191)
         du = e.d < cur ? e.d : cur;
@@ -1328,11 +1352,13 @@ struct Worker {
   __device__ int read_cascade() {
     unsigned long long t0 = pclk();
     if (l0size > 0) {
+      last_src = 1;
       const int c = l0_read(batch, L);
       count(M_L0D, (unsigned long long)c);
       pacc(P_L0L1, t0);
       return c;
     }
+    last_src = 2;
     const int c1 = l1_read(batch, L);
     pacc(P_L0L1, t0);
     if (c1 > 0) {
@@ -1346,6 +1372,7 @@ struct Worker {
     }
     pacc(P_HUB, t0);
     t0 = pclk();
+    last_src = 3;
     const int c2 = l2_read(batch);
     pacc(P_L2R, t0);
     return c2;

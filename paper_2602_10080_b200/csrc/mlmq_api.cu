@@ -520,6 +520,12 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     set_last_error("hub work ring slot %llu stayed busy for %gs (capacity %llu)", au[9], spin, au[11]);
     return MLMQ_EOVERFLOW;
   }
+  if (err == ERR_CORRUPT) {
+    w.dirty = true;
+    set_last_error("internal error: corrupt queue state code=%llu value=%llu (n=%llu) group=%llu extra=%llu",
+                   au[8], au[9], g->n, au[10], au[11]);
+    return MLMQ_EENGINE;
+  }
   if (err == 99) {
     w.dirty = true;
     set_last_error("queue ring state inconsistent at solve start");
