@@ -104,8 +104,15 @@ struct Worker {
   __device__ __forceinline__ void wstate(int code, unsigned long long tk) {
     if (p.wstate) p.wstate[gid] = ((unsigned long long)code << 56) | (tk & ((1ull << 56) - 1));
   }
+  // per-lane check, only for spins that a single lane runs
   __device__ __forceinline__ bool stopped() const {
     return ld_relaxed(p.ctl + C_STOP) != 0;
+  }
+  // warp-uniform check (lane 0 loads, everyone agrees) for warp control flow
+  __device__ __forceinline__ bool stopped_warp() const {
+    int s = 0;
+    if (lane == 0) s = ld_relaxed(p.ctl + C_STOP) != 0;
+    return __shfl_sync(FULL, s, 0) != 0;
   }
   __device__ __forceinline__ unsigned long long* wp(int r) const { return p.ptrs + (size_t)r * 32; }
   __device__ __forceinline__ unsigned long long* rp(int r) const { return p.ptrs + (size_t)r * 32 + 16; }
@@ -407,7 +414,7 @@ struct Worker {
     if (!p.bscratch) {  // very wide windows: per-round grouping
       for (int o = 0; o < n; o += 32) {
         const bool has = o + lane < n;
-        E x;
+        E x = E();
         int f = 0;
         if (has) {
           x = base[(start + o + lane) % cap];
@@ -489,7 +496,7 @@ struct Worker {
         int kept = 0;
         for (int o = 0; o < c; o += 32) {
           const bool has = o + lane < c;
-          E x;
+          E x = E();
           int rel = 0;
           if (has) {
             x = dst[o + lane];
@@ -506,7 +513,7 @@ struct Worker {
           __syncwarp();
         }
         if (kept > 0) return kept;
-        if (stopped()) return 0;
+        if (stopped_warp()) return 0;
       }
     }
     if (head_empty) {
@@ -629,7 +636,7 @@ struct Worker {
     for (int o = 0; o < n; o += 32) {
       const int c = min(32, n - o);
       const bool has = lane < c;
-      E x;
+      E x = E();
       if (has) x = base[(start + o + lane) % cap];
       warp_sort(x, has);
       const int nb = p.nb;
@@ -688,7 +695,7 @@ struct Worker {
       if (lane < t) dst[n + lane] = e;
       n += t;
       const int rem = c0 - t;
-      E sh;
+      E sh = E();
       sh.v = __shfl_sync(FULL, e.v, (lane + t) & 31);
       sh.d = __shfl_sync(FULL, e.d, (lane + t) & 31);
       __syncwarp();
@@ -841,7 +848,7 @@ struct Worker {
     int adm_seen = 0, back = 0;
     for (int o = 0; o < ns; o += 32) {
       const bool has = o + lane < ns;
-      E x;
+      E x = E();
       if (has) x = spill[o + lane];
       __syncwarp();
       const bool adm = has && x.d <= thr;
@@ -885,7 +892,7 @@ struct Worker {
     int ns_seen = 0, fs_seen = 0, back = 0;
     for (int o = 0; o < ns; o += 32) {
       const bool has = o + lane < ns;
-      E x;
+      E x = E();
       if (has) x = spill[o + lane];
       __syncwarp();
       const bool nr = has && x.d < thr;
@@ -935,7 +942,7 @@ struct Worker {
     int f_seen = 0, b_seen = 0, back = 0;
     for (int o = 0; o < ns; o += 32) {
       const bool has = o + lane < ns;
-      E x;
+      E x = E();
       if (has) x = spill[o + lane];
       __syncwarp();
       const bool fr = has && x.d < hd;
@@ -992,7 +999,7 @@ struct Worker {
         int kf = 0;
         for (int o = 0; o < n2; o += 32) {
           const bool has = o + lane < n2;
-          E x;
+          E x = E();
           if (has) x = l1b[ridx(h2, o + lane, cap)];
           __syncwarp();
           const bool nr = has && x.d < thr;
@@ -1024,7 +1031,7 @@ struct Worker {
   // the unplaced remainder into L1; L1's write-back goes through to L2.
   __device__ void cascade_write(const E* src, int k) {
     const bool has = lane < k;
-    E b;
+    E b = E();
     if (has) b = src[lane];
     const bool isfull = lane < L && l0n >= p.l0cap;
     const unsigned fullmask = __ballot_sync(FULL, isfull);
@@ -1082,8 +1089,8 @@ struct Worker {
   // engine.py:201-220 per edge: nd = dist[u] + w; if nd < dist[v] and atomic-min
   // improves (core.py:205-213): emit (v, nd).
   __device__ void relax_slots(bool (&act)[U], const unsigned long long (&kk)[U], const S (&du)[U]) {
-    uint32_t v[U];
-    S nd[U];
+    uint32_t v[U] = {0, 0, 0, 0};
+    S nd[U] = {0, 0, 0, 0};
     int c = 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
@@ -1202,7 +1209,7 @@ struct Worker {
     if (!got) return false;
     r = __shfl_sync(FULL, r, 0);
     const unsigned long long slot = r & p.hub_mask;
-    HubItem it;
+    HubItem it = HubItem();
     int ok = 1;
     if (lane == 0) {
       wstate(W_HUB_READ, r + 1);
@@ -1244,7 +1251,7 @@ struct Worker {
     for (int base = 0; base < nb; base += 32) {
       const int i = base + lane;
       bool valid = i < nb;
-      E e;
+      E e = E();
       S du = (S)Tr::INF;
       unsigned long long lo = 0, hi = 0;
       if (valid) {
@@ -1382,7 +1389,7 @@ struct Worker {
     int backoff = 0;
     const unsigned long long tstart = pclk();
     for (;;) {
-      if (stopped()) break;
+      if (stopped_warp()) break;
       const int c = read_cascade();
       if (c != 0 && idle) {
         idle = false;
@@ -1446,8 +1453,14 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
       st_release(p.ctl + C_STOP, 1ull);
     }
     __syncwarp();
-    if (ld_relaxed(p.ctl + C_STOP) != 0ull) break;
-    const unsigned long long d = ld_acquire(p.ctl + C_DONE);
+    int st = 0;
+    unsigned long long d = 0;
+    if (lane == 0) {
+      st = ld_relaxed(p.ctl + C_STOP) != 0ull;
+      d = ld_acquire(p.ctl + C_DONE);
+    }
+    if (__shfl_sync(FULL, st, 0)) break;
+    d = __shfl_sync(FULL, d, 0);
     unsigned long long r = 0;
     for (int i = lane; i < p.nrings; i += 32) r += ld_relaxed(p.ptrs + (size_t)i * 32);
     for (int i = lane; i < p.pnum; i += 32) r += ld_relaxed(p.hwc + (size_t)i * 16);
