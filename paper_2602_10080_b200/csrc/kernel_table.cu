@@ -1,29 +1,18 @@
-// kernel_table.cu — instantiations of K1 for one distance kind per translation unit.
-// Compiled three times with -DMLMQ_DK=0/1/2 (u32 / u64 / f32) so nvcc runs in parallel.
+// kernel_table.cu — one K1 instantiation per translation unit (distance kind x L2 family x
+// L0 register capacity), compiled with -DMLMQ_DK/-DMLMQ_L2K/-DMLMQ_CM so nvcc runs in parallel.
 #include "kernels/mlmq_kernel.cuh"
 
-#ifndef MLMQ_DK
-#error "define MLMQ_DK"
+#if !defined(MLMQ_DK) || !defined(MLMQ_L2K) || !defined(MLMQ_CM)
+#error "define MLMQ_DK, MLMQ_L2K and MLMQ_CM"
 #endif
 
 namespace mlmq {
 
-#define MLMQ_KFN_NAME_(k) kernel_for_dk##k
-#define MLMQ_KFN_NAME(k) MLMQ_KFN_NAME_(k)
+#define MLMQ_KFN_NAME_(d, l, c) kernel_dk##d##_l##l##_c##c
+#define MLMQ_KFN_NAME(d, l, c) MLMQ_KFN_NAME_(d, l, c)
 
-const void* MLMQ_KFN_NAME(MLMQ_DK)(int l2k, int cm) {
-  if (cm <= 4) {
-    switch (l2k) {
-      case L2K_FIFO: return (const void*)mlmq_persistent_kernel<MLMQ_DK, L2K_FIFO, 4>;
-      case L2K_BUCKET: return (const void*)mlmq_persistent_kernel<MLMQ_DK, L2K_BUCKET, 4>;
-      default: return (const void*)mlmq_persistent_kernel<MLMQ_DK, L2K_HEAP, 4>;
-    }
-  }
-  switch (l2k) {
-    case L2K_FIFO: return (const void*)mlmq_persistent_kernel<MLMQ_DK, L2K_FIFO, 16>;
-    case L2K_BUCKET: return (const void*)mlmq_persistent_kernel<MLMQ_DK, L2K_BUCKET, 16>;
-    default: return (const void*)mlmq_persistent_kernel<MLMQ_DK, L2K_HEAP, 16>;
-  }
+const void* MLMQ_KFN_NAME(MLMQ_DK, MLMQ_L2K, MLMQ_CM)() {
+  return (const void*)mlmq_persistent_kernel<MLMQ_DK, MLMQ_L2K, MLMQ_CM>;
 }
 
 }  // namespace mlmq

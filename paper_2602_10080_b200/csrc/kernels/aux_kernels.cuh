@@ -105,6 +105,7 @@ __global__ void audit_kernel(KParams p, unsigned long long* out, int fifo_fix) {
   }
   if (t == 0) {
     const unsigned long long* ctl = p.ctl;
+    if (p.wstate) p.wstate[2 * (size_t)p.G + 5] = 1;
     out[0] = ctl[C_DONE];
     out[1] = s_res[0] + ctl[C_HUB_WP];
     out[2] = s_bad[0];
@@ -122,6 +123,7 @@ __global__ void audit_kernel(KParams p, unsigned long long* out, int fifo_fix) {
       if (rd > w) p.ptrs[0] = rd;
       __threadfence();
     }
+    if (p.wstate) p.wstate[2 * (size_t)p.G + 5] = 2;
   }
 }
 

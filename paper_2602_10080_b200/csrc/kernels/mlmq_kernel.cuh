@@ -101,6 +101,38 @@ struct Worker {
   __device__ __forceinline__ void pcnt(int slot, unsigned long long v) {
     if (p.prof && lane == 0) met[kProfBase + slot] += v;
   }
+// Per-lane source-line trace (build with -DMLMQ_TRACE, run with MLMQ_DEBUG=1): the stuck
+// dump prints every lane's last line, which exposes lanes that left warp-uniform flow.
+#ifdef MLMQ_TRACE
+#define LOC() trace(__LINE__)
+#else
+#define LOC() ((void)0)
+#endif
+#define CHKU() check_uniform(__LINE__)
+  // debug: every "warp-uniform" scalar of the worker must agree with lane 0
+  __device__ void check_uniform(int line) {
+    if (!p.wstate) return;
+    unsigned long long h = (unsigned long long)l0size ^ ((unsigned long long)n1 << 13) ^
+                           ((unsigned long long)n2 << 26) ^ ((unsigned long long)outn << 39) ^
+                           ((unsigned long long)h1 << 45) ^ ((unsigned long long)h2 << 51) ^
+                           ((unsigned long long)wc << 57) ^ ((unsigned long long)rc << 3) ^
+                           ((unsigned long long)thr * 0x9E3779B97F4A7C15ull) ^ (local_done * 0x100000001B3ull) ^
+                           ((unsigned long long)wcount << 20) ^ ((unsigned long long)idle << 62) ^
+                           ((unsigned long long)has_rej << 61) ^ ((unsigned long long)rej_min * 31ull);
+    const unsigned long long h0 = __shfl_sync(FULL, h, 0);
+    const unsigned bad = __ballot_sync(FULL, h != h0);
+    if (bad && lane == 0) raise_error(ERR_CORRUPT, 7000000ull + line, bad, (unsigned long long)gid, h0);
+  }
+  __device__ __forceinline__ void trace(int line) {
+    if (p.wstate) p.wstate[2 * (size_t)p.G + 8 + (size_t)gid * 32 + lane] = (unsigned long long)line;
+  }
+  // debug: where the warp is and its local queue sizes (wstate[G + gid])
+  __device__ __forceinline__ void loc(int ph) {
+    if (p.wstate && lane == 0)
+      p.wstate[p.G + gid] = ((unsigned long long)ph << 56) | ((unsigned long long)(l0size & 0xFFFF) << 40) |
+                            ((unsigned long long)(n1 & 0xFFFF) << 24) | ((unsigned long long)(n2 & 0xFFF) << 12) |
+                            (unsigned long long)(outn & 0xFFF);
+  }
   __device__ __forceinline__ void wstate(int code, unsigned long long tk) {
     if (p.wstate) p.wstate[gid] = ((unsigned long long)code << 56) | (tk & ((1ull << 56) - 1));
   }
@@ -113,6 +145,14 @@ struct Worker {
     int s = 0;
     if (lane == 0) s = ld_relaxed(p.ctl + C_STOP) != 0;
     return __shfl_sync(FULL, s, 0) != 0;
+  }
+  // A global word read by lane 0 and broadcast: concurrent writers can make a warp-wide
+  // load of one address return different values to different lanes, so every global
+  // value that steers warp control flow is read this way.
+  __device__ __forceinline__ unsigned long long warp_ld(const unsigned long long* a) const {
+    unsigned long long v = 0;
+    if (lane == 0) v = ld_relaxed(a);
+    return __shfl_sync(FULL, v, 0);
   }
   __device__ __forceinline__ unsigned long long* wp(int r) const { return p.ptrs + (size_t)r * 32; }
   __device__ __forceinline__ unsigned long long* rp(int r) const { return p.ptrs + (size_t)r * 32 + 16; }
@@ -148,6 +188,7 @@ struct Worker {
   // Drain every lane, lanes in round-robin order from the read cursor, each lane FIFO
   // (l1.py:87-96).  Returns the number of elements written to dst.
   __device__ int l0_drain(E* dst) {
+    LOC();
     const int q = lane;
     const int srcl = (rc + q) % L;
     int c = __shfl_sync(FULL, l0n, srcl);
@@ -175,11 +216,14 @@ struct Worker {
   // Pop up to `want`, one per non-empty lane per round from the read cursor
   // (l1.py:66-85); the cursor ends after the lane that gave the last element.
   __device__ int l0_read(E* dst, int want) {
+    LOC();
+    loc(11);
     const int T = min(want, l0size);
     int taken = 0, last = 0;
     const unsigned lmask = (L == 32) ? FULL : ((1u << L) - 1u);
     const int r = (lane - rc + L) % L;
     while (taken < T) {
+      LOC();
       const bool ne = lane < L && l0n > 0;
       const unsigned m = __ballot_sync(FULL, ne);
       const unsigned rot = rc == 0 ? m : (((m >> rc) | (m << (L - rc))) & lmask);
@@ -203,6 +247,7 @@ struct Worker {
     rc = (last + 1) % L;
     l0size -= T;
     __syncwarp();
+    CHKU();
     return T;
   }
 
@@ -223,6 +268,7 @@ struct Worker {
     unsigned long long t0 = 0;
     int spins = 0, ns = 32;
     while (ld_acquire(s) != want) {
+      LOC();
       if (++spins % 64 == 0) {
         if (stopped()) return false;
         const unsigned long long now = globaltimer_ns();
@@ -241,9 +287,11 @@ struct Worker {
 
   // Wait (lanes in parallel) until the nseg slots of tickets t..t+nseg-1 are free.
   __device__ bool wait_free(int rid, unsigned long long t, int nseg) {
+    LOC();
     bool ok = true;
     if (lane == 0) wstate(W_RING_WRITE, t);
     for (int sg = lane; sg < nseg; sg += 32) {
+      LOC();
       const unsigned long long tk = t + sg, slot = tk & p.bn_mask;
       if (ok && !lane_spin(seq_ptr(rid, slot), tk, rid, slot)) ok = false;
     }
@@ -254,9 +302,11 @@ struct Worker {
 
   // Publish (lanes in parallel) the nseg blocks of tickets t.. holding `n` elements.
   __device__ void publish_all(int rid, unsigned long long t, int nseg, int n) {
+    LOC();
     __threadfence();
     __syncwarp();
     for (int sg = lane; sg < nseg; sg += 32) {
+      LOC();
       const unsigned long long tk = t + sg, slot = tk & p.bn_mask;
       const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
       p.cnt[i] = (uint32_t)min(p.bs, n - sg * p.bs);
@@ -268,6 +318,7 @@ struct Worker {
   // Writer (l2.py:96-114): one fetch-add claims ceil(n/bs) tickets; all slot waits,
   // element stores and publications of the write proceed warp-parallel.
   __device__ void ring_write(int rid, const E* base, int start, int n, int cap) {
+    LOC();
     if (n <= 0) return;
     const int bs = p.bs;
     const int nseg = (n + bs - 1) / bs;
@@ -277,6 +328,7 @@ struct Worker {
     count(M_L2A, 1);
     if (!wait_free(rid, t, nseg)) return;
     for (int i = lane; i < n; i += 32) {
+      LOC();
       const int sg = i / bs;
       slot_data(rid, (t + sg) & p.bn_mask)[i - sg * bs] = base[(start + i) % cap];
     }
@@ -285,6 +337,7 @@ struct Worker {
 
   // Same, with the elements held one per lane (grp = writing lanes, rank within grp).
   __device__ void ring_write_lanes(int rid, unsigned grp, int rank, const E& x, bool mine) {
+    LOC();
     const int c = __popc(grp);
     const int bs = p.bs;
     const int nseg = (c + bs - 1) / bs;
@@ -302,6 +355,7 @@ struct Worker {
 
   // Copy ticket r's published block out and free the slot.
   __device__ int take_block(int rid, unsigned long long r, E* dst) {
+    LOC();
     const unsigned long long slot = r & p.bn_mask;
     const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
     int c = 0;
@@ -322,6 +376,7 @@ struct Worker {
   // Conditional reader (l2.py:137-162): claim a ticket only when a written block
   // exists, then wait for the in-flight writer; never leaves a dangling claim.
   __device__ int ring_read(int rid, E* dst) {
+    LOC();
     unsigned long long r = 0;
     int got = 0;
     if (lane == 0) {
@@ -330,6 +385,7 @@ struct Worker {
       r = ld_relaxed(rpp);
       unsigned long long w = ld_relaxed(wpp);
       while (r < w) {
+        LOC();
         unsigned long long old = atomicCAS(rpp, r, r + 1);
         if (old == r) { got = 1; break; }
         if (p.prof) met[kProfBase + P_CASFAIL] += 1;
@@ -359,6 +415,7 @@ struct Worker {
   // Tickets still pending at termination are retired by the audit kernel.
   unsigned long long pend;
   __device__ int fifo_read(E* dst) {
+    LOC();
     if (pend == ~0ull) {
       unsigned long long r = 0;
       if (lane == 0) r = atomicAdd(rp(0), 1ull);
@@ -393,8 +450,10 @@ struct Worker {
 
   // Group the lanes' elements by target bucket ring and write each group as blocks.
   __device__ void bucket_scatter_lanes(bool has, const E& x, int f) {
+    LOC();
     unsigned act = __ballot_sync(FULL, has);
     while (act) {
+      LOC();
       const int leader = __ffs(act) - 1;
       const int fl = __shfl_sync(FULL, f, leader);
       const bool mine = has && f == fl;
@@ -409,10 +468,12 @@ struct Worker {
   // Warp-parallel: (1) per-bucket histogram in shared memory, (2) one ticket fetch-add
   // per non-empty bucket, (3) parallel slot waits, (4) scatter, (5) parallel publish.
   __device__ void bucket_write(const E* base, int start, int n, int cap) {
-    const unsigned long long e = ld_relaxed(p.ctl + C_EPOCH);
+    LOC();
+    const unsigned long long e = warp_ld(p.ctl + C_EPOCH);
     const unsigned long long bm = (unsigned long long)p.bmax;
     if (!p.bscratch) {  // very wide windows: per-round grouping
       for (int o = 0; o < n; o += 32) {
+        LOC();
         const bool has = o + lane < n;
         E x = E();
         int f = 0;
@@ -428,12 +489,14 @@ struct Worker {
     for (int b = lane; b < p.bmax; b += 32) { bhist[b] = 0; bcur[b] = 0; }
     __syncwarp();
     for (int i = lane; i < n; i += 32) {
+      LOC();
       const E x = base[(start + i) % cap];
       atomicAdd(bhist + (int)((e + (unsigned long long)bucket_rel(x.d, e)) % bm), 1u);
     }
     __syncwarp();
     int used = 0;
     for (int b = lane; b < p.bmax; b += 32) {
+      LOC();
       const int c = (int)bhist[b];
       if (c) {
         btick[b] = atomicAdd(wp(b), (unsigned long long)((c + bs - 1) / bs));
@@ -445,9 +508,11 @@ struct Worker {
     bool ok = true;
     if (lane == 0) wstate(W_RING_WRITE, e);
     for (int b = lane; b < p.bmax; b += 32) {
+      LOC();
       const int c = (int)bhist[b];
       const int nseg = (c + bs - 1) / bs;
       for (int sg = 0; ok && sg < nseg; ++sg) {
+        LOC();
         const unsigned long long tk = btick[b] + sg, slot = tk & p.bn_mask;
         ok = lane_spin(seq_ptr(b, slot), tk, b, slot);
       }
@@ -455,6 +520,7 @@ struct Worker {
     if (lane == 0) wstate(W_NONE, 0);
     if (!__all_sync(FULL, ok)) return;
     for (int i = lane; i < n; i += 32) {
+      LOC();
       const E x = base[(start + i) % cap];
       const int f = (int)((e + (unsigned long long)bucket_rel(x.d, e)) % bm);
       const int r = (int)atomicAdd(bcur + f, 1u);
@@ -464,9 +530,11 @@ struct Worker {
     __threadfence();
     __syncwarp();
     for (int b = lane; b < p.bmax; b += 32) {
+      LOC();
       const int c = (int)bhist[b];
       const int nseg = (c + bs - 1) / bs;
       for (int sg = 0; sg < nseg; ++sg) {
+        LOC();
         const unsigned long long tk = btick[b] + sg, slot = tk & p.bn_mask;
         const size_t i = (size_t)b * (p.bn_mask + 1) + slot;
         p.cnt[i] = (uint32_t)min(bs, c - sg * bs);
@@ -479,22 +547,27 @@ struct Worker {
   // l2.py:235-295: scan bnum buckets from the floor; rebin stale-slot elements; advance
   // the floor by one when the head is seen empty while elements remain elsewhere.
   __device__ int bucket_read(E* dst) {
-    const unsigned long long e0 = ld_relaxed(p.ctl + C_EPOCH);
+    LOC();
+    loc(16);
+    const unsigned long long e0 = warp_ld(p.ctl + C_EPOCH);
     bool head_empty = false;
     for (int j = 0; j < p.bnum; ++j) {
+      LOC();
       const int f = (int)((e0 + (unsigned long long)j) % (unsigned long long)p.bmax);
       for (;;) {
+        LOC();
         const int c = ring_read(f, dst);
         if (c == 0) {
           if (j == 0) head_empty = true;
           break;
         }
         local_done += 1;
-        const unsigned long long en = ld_relaxed(p.ctl + C_EPOCH);
+        const unsigned long long en = warp_ld(p.ctl + C_EPOCH);
         const int rel_slot = (int)(((unsigned long long)f + (unsigned long long)p.bmax -
                                     (en % (unsigned long long)p.bmax)) % (unsigned long long)p.bmax);
         int kept = 0;
         for (int o = 0; o < c; o += 32) {
+          LOC();
           const bool has = o + lane < c;
           E x = E();
           int rel = 0;
@@ -541,6 +614,7 @@ struct Worker {
     return __shfl_sync(FULL, v, 0);
   }
   __device__ void node_swap(int h, unsigned long long a, unsigned long long b) {
+    LOC();
     E* A = node_elems(h, a);
     E* B = node_elems(h, b);
     E xa = ld_cg_elem(A + lane), xb = ld_cg_elem(B + lane);
@@ -554,6 +628,7 @@ struct Worker {
     __syncwarp();
   }
   __device__ bool heap_lock(int h) {
+    LOC();
     int ok = 1;
     if (lane == 0) {
       uint32_t* lk = p.hlock + (size_t)h * 32;
@@ -561,6 +636,7 @@ struct Worker {
       unsigned long long t0 = 0;
       int spins = 0, ns = 32;
       while (atomicCAS(lk, 0u, 1u) != 0u) {
+        LOC();
         if (++spins % 64 == 0) {
           if (stopped()) { ok = 0; break; }
           unsigned long long now = globaltimer_ns();
@@ -582,12 +658,15 @@ struct Worker {
     return ok != 0;
   }
   __device__ void heap_unlock(int h) {
+    LOC();
     __threadfence();
     __syncwarp();
     if (lane == 0) atomicExch(p.hlock + (size_t)h * 32, 0u);
   }
   __device__ void sift_up(int h, unsigned long long i) {
+    LOC();
     while (i > 0) {
+      LOC();
       const unsigned long long par = (i - 1) >> 1;
       if (node_min(h, i) < node_min(h, par)) {
         node_swap(h, i, par);
@@ -597,7 +676,9 @@ struct Worker {
     }
   }
   __device__ void sift_down(int h, unsigned long long i, unsigned long long size) {
+    LOC();
     for (;;) {
+      LOC();
       unsigned long long c = 2 * i + 1;
       if (c >= size) return;
       if (c + 1 < size && node_min(h, c + 1) < node_min(h, c)) ++c;
@@ -613,12 +694,15 @@ struct Worker {
   }
   // bitonic sort of one element per lane (invalid lanes sort last)
   __device__ void warp_sort(E& x, bool has) {
+    LOC();
     S d = has ? x.d : (S)Tr::INF;
     uint32_t v = has ? x.v : 0xFFFFFFFFu;
 #pragma unroll
     for (int k = 2; k <= 32; k <<= 1) {
+      LOC();
 #pragma unroll
       for (int j = k >> 1; j > 0; j >>= 1) {
+        LOC();
         const S pd = __shfl_xor_sync(FULL, d, j);
         const uint32_t pv = __shfl_xor_sync(FULL, v, j);
         const bool up = (lane & k) == 0;
@@ -633,7 +717,9 @@ struct Worker {
   }
   // l2.py:322-344: sorted batch -> nodes of <= node_batch, appended as leaves + sift-up.
   __device__ void heap_write(int h, const E* base, int start, int n, int cap) {
+    LOC();
     for (int o = 0; o < n; o += 32) {
+      LOC();
       const int c = min(32, n - o);
       const bool has = lane < c;
       E x = E();
@@ -651,6 +737,7 @@ struct Worker {
         return;
       }
       for (int q = 0; q < nn; ++q) {
+        LOC();
         const unsigned long long i = size + (unsigned long long)q;
         if (has && lane / nb == q) node_elems(h, i)[lane % nb] = x;
         if (lane == 0) *node_cnt(h, i) = (uint32_t)min(nb, c - q * nb);
@@ -669,6 +756,7 @@ struct Worker {
   }
   // l2.py:362-389: pop runs off the root while root.min <= min(child mins).
   __device__ int heap_read(int h, E* dst, int want) {
+    LOC();
     if (lane == 0 && ld_relaxed(p.hsize + (size_t)h * 16) == 0) want = -1;
     if (__shfl_sync(FULL, want, 0) < 0) return 0;
     if (!heap_lock(h)) return 0;
@@ -677,6 +765,7 @@ struct Worker {
     size = __shfl_sync(FULL, size, 0);
     int n = 0;
     while (size > 0 && n < want) {
+      LOC();
       int c0 = 0;
       if (lane == 0) c0 = (int)__ldcg(node_cnt(h, 0));
       c0 = __shfl_sync(FULL, c0, 0);
@@ -735,6 +824,7 @@ struct Worker {
   // write_through (compose.py:79-86): the termination reservation is the ring ticket
   // (or heap write counter) itself, claimed before the block is published.
   __device__ void write_back(const E* base, int start, int n, int cap) {
+    LOC();
     if (n <= 0) return;
     const unsigned long long t0 = pclk();
     count(M_L2E, (unsigned long long)n);
@@ -752,6 +842,7 @@ struct Worker {
   }
 
   __device__ int l2_read(E* dst) {
+    LOC();
     int c;
     if (L2K == L2K_FIFO) {
       c = p.fifo_park ? fifo_read(dst) : ring_read(0, dst);
@@ -775,6 +866,7 @@ struct Worker {
 
   // pop min(want, size) from the front of a ring
   __device__ int ring_pop_front(E* ring, int& h, int& n, E* dst, int want) {
+    LOC();
     const int c = min(want, n);
     const int cap = p.l1cap;
     for (int i = lane; i < c; i += 32) dst[i] = ring[ridx(h, i, cap)];
@@ -786,6 +878,7 @@ struct Worker {
 
   // append spill[from..to) (predicate-filtered, stable) to the ring tail; returns count
   __device__ void ring_append(E* ring, int h, int& n, const E* src, int i0, int cnt) {
+    LOC();
     const int cap = p.l1cap;
     for (int i = lane; i < cnt; i += 32) ring[ridx(h, n + i, cap)] = src[i0 + i];
     n += cnt;
@@ -795,6 +888,7 @@ struct Worker {
   // L1 Vector write (l1.py:116-129): append, evict the front over capacity, flush all
   // after every wb write invocations.
   __device__ void l1_vector_write(int ns) {
+    LOC();
     const int cap = p.l1cap;
     const int total = n1 + ns;
     const int evict = max(0, total - cap);
@@ -819,10 +913,12 @@ struct Worker {
   // L1 Filter write (l1.py:213-230): admit d <= F, reject to L2 tracking reject_min,
   // evict the front over capacity.
   __device__ void l1_filter_write(int ns) {
+    LOC();
     const int cap = p.l1cap;
     int A = 0;
     S rmin = rej_min;
     for (int o = 0; o < ns; o += 32) {
+      LOC();
       const bool has = o + lane < ns;
       S d = has ? spill[o + lane].d : (S)0;
       const bool adm = has && d <= thr;
@@ -830,6 +926,7 @@ struct Worker {
       S rd = (has && !adm) ? d : (S)Tr::INF;
 #pragma unroll
       for (int k = 16; k > 0; k >>= 1) {
+        LOC();
         S t = __shfl_xor_sync(FULL, rd, k);
         rd = t < rd ? t : rd;
       }
@@ -847,6 +944,7 @@ struct Worker {
     // first `en` admitted are compacted to the spill front and written back
     int adm_seen = 0, back = 0;
     for (int o = 0; o < ns; o += 32) {
+      LOC();
       const bool has = o + lane < ns;
       E x = E();
       if (has) x = spill[o + lane];
@@ -873,9 +971,11 @@ struct Worker {
   // L1 NearFar write (l1.py:157-177): partition by d < NF; over capacity evict
   // far-front first, then near-front.
   __device__ void l1_nearfar_write(int ns) {
+    LOC();
     const int cap = p.l1cap;
     int Nn = 0;
     for (int o = 0; o < ns; o += 32) {
+      LOC();
       const bool has = o + lane < ns;
       const bool nr = has && spill[o + lane].d < thr;
       Nn += __popc(__ballot_sync(FULL, nr));
@@ -891,6 +991,7 @@ struct Worker {
     if (enr) { write_back(l1a, h1, enr, cap); h1 = ridx(h1, enr, cap); n1 -= enr; }
     int ns_seen = 0, fs_seen = 0, back = 0;
     for (int o = 0; o < ns; o += 32) {
+      LOC();
       const bool has = o + lane < ns;
       E x = E();
       if (has) x = spill[o + lane];
@@ -923,11 +1024,13 @@ struct Worker {
   // L1 SLF write (l1.py:263-274): head distance snapshot; shorter -> push front
   // (reversing arrival order), else push back; over capacity pop from the tail.
   __device__ void l1_slf_write(int ns) {
+    LOC();
     const int cap = p.l1cap;
     S hd = (S)Tr::INF;
     if (n1 > 0) hd = l1a[h1].d;
     int pf = 0;
     for (int o = 0; o < ns; o += 32) {
+      LOC();
       const bool has = o + lane < ns;
       pf += __popc(__ballot_sync(FULL, has && spill[o + lane].d < hd));
     }
@@ -941,6 +1044,7 @@ struct Worker {
     const int sb = max(0, cap - pf - n1);  // surviving back pushers
     int f_seen = 0, b_seen = 0, back = 0;
     for (int o = 0; o < ns; o += 32) {
+      LOC();
       const bool has = o + lane < ns;
       E x = E();
       if (has) x = spill[o + lane];
@@ -970,6 +1074,7 @@ struct Worker {
   }
 
   __device__ void l1_write(int ns) {
+    LOC();
     switch (p.l1type) {
       case L1K_VECTOR: l1_vector_write(ns); break;
       case L1K_NEAR_FAR: l1_nearfar_write(ns); break;
@@ -980,16 +1085,20 @@ struct Worker {
 
   // L1 reads (l1.py:131-136, 179-189, 232-242, 276-280)
   __device__ int l1_read(E* dst, int want) {
+    LOC();
+    loc(12);
     const int cap = p.l1cap;
     if (p.l1type == L1K_NEAR_FAR) {
       if (n1 == 0 && n2 > 0) {
         S mn = (S)Tr::INF;
         for (int i = lane; i < n2; i += 32) {
+          LOC();
           const S d = l1b[ridx(h2, i, cap)].d;
           mn = d < mn ? d : mn;
         }
 #pragma unroll
         for (int k = 16; k > 0; k >>= 1) {
+          LOC();
           S t = __shfl_xor_sync(FULL, mn, k);
           mn = t < mn ? t : mn;
         }
@@ -998,6 +1107,7 @@ struct Worker {
         h1 = 0;
         int kf = 0;
         for (int o = 0; o < n2; o += 32) {
+          LOC();
           const bool has = o + lane < n2;
           E x = E();
           if (has) x = l1b[ridx(h2, o + lane, cap)];
@@ -1030,6 +1140,8 @@ struct Worker {
   // compose.py:56-77: L0.write; a full target lane triggers a full transfer of L0 plus
   // the unplaced remainder into L1; L1's write-back goes through to L2.
   __device__ void cascade_write(const E* src, int k) {
+    LOC();
+    loc(14);
     const bool has = lane < k;
     E b = E();
     if (has) b = src[lane];
@@ -1047,6 +1159,7 @@ struct Worker {
     if (f == k) {
       wc = (wc + k) % L;
       l0size += k;
+      CHKU();
       return;
     }
     const int before = l0size;
@@ -1061,12 +1174,16 @@ struct Worker {
     l0size = 0;
     count(M_L0D, (unsigned long long)(before + f));
     __syncwarp();
+    CHKU();
     l1_write(ns);
+    CHKU();
   }
 
   __device__ void flush_out(bool all) {
+    LOC();
     int d = 0;
     while (outn - d >= L) {
+      LOC();
       cascade_write(outs + d, L);
       d += L;
     }
@@ -1089,11 +1206,13 @@ struct Worker {
   // engine.py:201-220 per edge: nd = dist[u] + w; if nd < dist[v] and atomic-min
   // improves (core.py:205-213): emit (v, nd).
   __device__ void relax_slots(bool (&act)[U], const unsigned long long (&kk)[U], const S (&du)[U]) {
+    LOC();
     uint32_t v[U] = {0, 0, 0, 0};
     S nd[U] = {0, 0, 0, 0};
     int c = 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
+      LOC();
       if (act[j]) {
         const uint2 a = __ldg(p.adj + kk[j]);
         v[j] = a.x;
@@ -1116,6 +1235,7 @@ struct Worker {
     int upd = 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
+      LOC();
       const unsigned m = __ballot_sync(FULL, act[j]);
       if (act[j]) {
         E e;
@@ -1134,12 +1254,15 @@ struct Worker {
 
   // the whole warp strides one edge list (engine.py:212-220 "big" tier, hub chunks)
   __device__ void relax_range(unsigned long long lo, unsigned long long hi, S du) {
+    LOC();
     const S dus[U] = {du, du, du, du};
     for (unsigned long long k0 = lo; k0 < hi; k0 += 32 * U) {
+      LOC();
       bool act[U];
       unsigned long long kk[U];
 #pragma unroll
       for (int j = 0; j < U; ++j) {
+        LOC();
         kk[j] = k0 + (unsigned long long)(j * 32 + lane);
         act[j] = kk[j] < hi;
       }
@@ -1148,6 +1271,7 @@ struct Worker {
   }
 
   __device__ void push_hub(uint32_t u, S du, unsigned long long lo, unsigned long long hi) {
+    LOC();
     const unsigned long long ch = p.hub_chunk;
     const unsigned long long nch = (hi - lo + ch - 1) / ch;
     unsigned long long t = 0;
@@ -1158,11 +1282,13 @@ struct Worker {
     t = __shfl_sync(FULL, t, 0);
     const unsigned long long cap = p.hub_mask + 1;
     for (unsigned long long q = lane; q < nch; q += 32) {
+      LOC();
       const unsigned long long tk = t + q, slot = tk & p.hub_mask;
       unsigned long long t0 = 0;
       int spins = 0;
       bool ok = true;
       while (ld_acquire(p.hub_seq + slot) != tk) {
+        LOC();
         if (++spins % 64 == 0) {
           if (stopped()) { ok = false; break; }
           unsigned long long now = globaltimer_ns();
@@ -1191,6 +1317,8 @@ struct Worker {
 
   // Claim one hub item if any; returns true and processes it.
   __device__ bool hub_try() {
+    LOC();
+    loc(17);
     unsigned long long r = 0;
     int got = 0;
     if (lane == 0) {
@@ -1199,6 +1327,7 @@ struct Worker {
       r = ld_relaxed(rpp);
       unsigned long long w = ld_relaxed(wpp);
       while (r < w) {
+        LOC();
         unsigned long long old = atomicCAS(rpp, r, r + 1);
         if (old == r) { got = 1; break; }
         r = old;
@@ -1214,6 +1343,7 @@ struct Worker {
     if (lane == 0) {
       wstate(W_HUB_READ, r + 1);
       while (ld_acquire(p.hub_seq + slot) != r + 1) {
+        LOC();
         if (stopped()) { ok = 0; break; }
         __nanosleep(64);
       }
@@ -1235,7 +1365,9 @@ struct Worker {
     it.u = __shfl_sync(FULL, it.u, 0);
     local_done += 1;
     S du = (S)it.du;
-    const S cur = ldcg_dist(dist + it.u);
+    S cur = 0;
+    if (lane == 0) cur = ldcg_dist(dist + it.u);
+    cur = __shfl_sync(FULL, cur, 0);
     if (p.dup && du > cur) return true;  // stale hub item (engine.py:190 analogue)
     if (cur < du) du = cur;
     relax_range(it.lo, it.hi, du);
@@ -1244,11 +1376,14 @@ struct Worker {
 
   // engine.py:171-227 for one batch in shared memory
   __device__ void relax_batch(int nb) {
+    LOC();
+    loc(13);
     if (nb > p.batch_cap) {
       if (lane == 0) raise_error(ERR_CORRUPT, 40, (unsigned long long)nb, (unsigned long long)gid, 0);
       return;
     }
     for (int base = 0; base < nb; base += 32) {
+      LOC();
       const int i = base + lane;
       bool valid = i < nb;
       E e = E();
@@ -1276,6 +1411,7 @@ struct Worker {
       // hub tier: split huge lists into shared edge-range items
       unsigned hm = __ballot_sync(FULL, valid && (hi - lo) > p.hub_thresh);
       while (hm) {
+        LOC();
         const int l = __ffs(hm) - 1;
         const uint32_t hu = __shfl_sync(FULL, e.v, l);
         const S hdu = __shfl_sync(FULL, du, l);
@@ -1294,15 +1430,18 @@ struct Worker {
       const int total = __shfl_sync(FULL, incl, 31);
       const int excl = incl - ds;
       for (int e0 = 0; e0 < total; e0 += 32 * U) {
+        LOC();
         bool act[U];
         unsigned long long kk[U];
         S dus[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
+          LOC();
           const int idx = e0 + j * 32 + lane;
           int o = 0;
 #pragma unroll
           for (int s = 16; s >= 1; s >>= 1) {
+            LOC();
             const int probe = __shfl_sync(FULL, incl, o + s - 1);
             if (probe <= idx) o += s;
           }
@@ -1317,6 +1456,7 @@ struct Worker {
       // big lists: the whole warp walks each one
       unsigned bm = __ballot_sync(FULL, big);
       while (bm) {
+        LOC();
         const int l = __ffs(bm) - 1;
         relax_range(__shfl_sync(FULL, lo, l), __shfl_sync(FULL, hi, l), __shfl_sync(FULL, du, l));
         bm &= bm - 1;
@@ -1331,7 +1471,9 @@ struct Worker {
   // holding more than two batches of local work writes its L1 (or, with L1 empty, its
   // L0) back to L2 where the idle groups can read it.
   __device__ void maybe_share() {
+    LOC();
     if (!p.share) return;
+    loc(15);
     const int local = l0size + n1 + n2;
     if (local <= 2 * L) return;
     unsigned long long idle_now = 0;
@@ -1357,6 +1499,7 @@ struct Worker {
   // compose.py:30-54. Returns >0 batch size, -1 when a hub item was processed, 0 on a
   // full miss.
   __device__ int read_cascade() {
+    LOC();
     unsigned long long t0 = pclk();
     if (l0size > 0) {
       last_src = 1;
@@ -1386,10 +1529,14 @@ struct Worker {
   }
 
   __device__ void run() {
+    LOC();
     int backoff = 0;
     const unsigned long long tstart = pclk();
     for (;;) {
+      LOC();
       if (stopped_warp()) break;
+      CHKU();
+      loc(10);
       const int c = read_cascade();
       if (c != 0 && idle) {
         idle = false;
@@ -1399,13 +1546,17 @@ struct Worker {
         const unsigned long long t0 = pclk();
         pcnt(P_NBATCH, 1);
         pcnt(P_BATCHSUM, (unsigned long long)c);
+        CHKU();
         relax_batch(c);
+        CHKU();
         pacc(P_RELAX, t0);
         maybe_share();
+        CHKU();
         backoff = 0;
         continue;
       }
       if (c < 0) {
+        CHKU();
         flush_out(true);
         maybe_share();
         backoff = 0;
@@ -1431,6 +1582,7 @@ struct Worker {
       pacc(P_IDLE, t0);
     }
     pacc(P_TOTAL, tstart);
+    loc(99);
     // exit: metric shard + audit evidence
     if (__any_sync(FULL, dist_ovf) && lane == 0) atomicOr(p.ctl + C_DIST_OVF, 1ull);
     const int l1size = n1 + n2;
@@ -1446,6 +1598,7 @@ struct Worker {
 // K2: manager warp (engine.py:152-169): reserve == done on three consecutive polls.
 static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
   int k = 0;
+  if (p.wstate && lane == 0) p.wstate[2 * (size_t)p.G + 4] = 1;
   for (;;) {
     if (p.host_abort && lane == 0 && ld_sys_u32(p.host_abort) != 0u) {
       atomicCAS(p.ctl + C_ERR, 0ull, (unsigned long long)ERR_ABORT);
@@ -1467,6 +1620,11 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
     if (lane == 0) r += ld_relaxed(p.ctl + C_HUB_WP);
     r = warp_sum_u64(r);
     k = (d == r) ? k + 1 : 0;
+    if (p.wstate && lane == 0) {
+      p.wstate[2 * (size_t)p.G] += 1;
+      p.wstate[2 * (size_t)p.G + 2] = d;
+      p.wstate[2 * (size_t)p.G + 3] = r;
+    }
     if (k >= 3) {
       if (lane == 0) st_release(p.ctl + C_STOP, 1ull);
       break;
@@ -1483,6 +1641,7 @@ __global__ void __launch_bounds__(256) mlmq_persistent_kernel(const __grid_const
   if (gid > p.G) return;
   if (gid == p.G) {
     manager_loop(p, lane);
+    if (p.wstate && lane == 0) p.wstate[2 * (size_t)p.G + 4] = 2;
     return;
   }
   Worker<K, L2K, CM> w(p, smem + (size_t)warp * p.smem_per_warp, gid, lane);

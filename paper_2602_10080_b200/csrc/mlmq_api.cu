@@ -25,9 +25,24 @@
 
 namespace mlmq {
 
-const void* kernel_for_dk0(int l2k, int cm);
-const void* kernel_for_dk1(int l2k, int cm);
-const void* kernel_for_dk2(int l2k, int cm);
+const void* kernel_dk0_l0_c4();
+const void* kernel_dk0_l0_c16();
+const void* kernel_dk0_l1_c4();
+const void* kernel_dk0_l1_c16();
+const void* kernel_dk0_l2_c4();
+const void* kernel_dk0_l2_c16();
+const void* kernel_dk1_l0_c4();
+const void* kernel_dk1_l0_c16();
+const void* kernel_dk1_l1_c4();
+const void* kernel_dk1_l1_c16();
+const void* kernel_dk1_l2_c4();
+const void* kernel_dk1_l2_c16();
+const void* kernel_dk2_l0_c4();
+const void* kernel_dk2_l0_c16();
+const void* kernel_dk2_l1_c4();
+const void* kernel_dk2_l1_c16();
+const void* kernel_dk2_l2_c4();
+const void* kernel_dk2_l2_c16();
 
 static thread_local char g_err[1024] = "";
 
@@ -128,11 +143,12 @@ struct mlmq_graph {
 namespace {
 
 const void* kernel_for(int dk, int l2k, int cm) {
-  switch (dk) {
-    case DK_U32: return kernel_for_dk0(l2k, cm);
-    case DK_U64: return kernel_for_dk1(l2k, cm);
-    default: return kernel_for_dk2(l2k, cm);
-  }
+  using Fn = const void* (*)();
+  static const Fn table[3][3][2] = {
+    {{kernel_dk0_l0_c4, kernel_dk0_l0_c16}, {kernel_dk0_l1_c4, kernel_dk0_l1_c16}, {kernel_dk0_l2_c4, kernel_dk0_l2_c16}},
+    {{kernel_dk1_l0_c4, kernel_dk1_l0_c16}, {kernel_dk1_l1_c4, kernel_dk1_l1_c16}, {kernel_dk1_l2_c4, kernel_dk1_l2_c16}},
+    {{kernel_dk2_l0_c4, kernel_dk2_l0_c16}, {kernel_dk2_l1_c4, kernel_dk2_l1_c16}, {kernel_dk2_l2_c4, kernel_dk2_l2_c16}}};
+  return table[dk][l2k][cm <= 4 ? 0 : 1]();
 }
 
 int l2_kind(int l2_type) {
@@ -304,9 +320,12 @@ bool debug_enabled() {
 
 // MLMQ_DEBUG=1: per-phase cycle breakdown and the wait states of stuck warps.
 void debug_dump(mlmq_graph* g, int G, const char* tag) {
-  std::vector<unsigned long long> pr((size_t)G * P_COUNT), ws((size_t)G);
+  std::vector<unsigned long long> pr((size_t)G * P_COUNT), ws((size_t)2 * G + 8 + (size_t)G * 32);
+  std::vector<unsigned long long> ctl(C_WORDS), ptr(64);
   if (cudaMemcpy(pr.data(), g->d_prof, pr.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
-      cudaMemcpy(ws.data(), g->d_wstate, ws.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaMemcpy(ws.data(), g->d_wstate, ws.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(ctl.data(), g->d_ctl, C_WORDS * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(ptr.data(), g->ws.ptrs, 32 * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
     cudaGetLastError();
     fprintf(stderr, "[mlmq debug] copy failed\n");
     return;
@@ -336,6 +355,40 @@ void debug_dump(mlmq_graph* g, int G, const char* tag) {
   }
   fprintf(stderr, "[mlmq debug]   wait states: none %d ringW %d ringR %d hubR %d hubW %d heap %d\n",
           hist[0], hist[1], hist[2], hist[3], hist[4], hist[5]);
+  int lh[128] = {0};
+  shown = 0;
+  for (int i = 0; i < G; ++i) {
+    const unsigned long long x = ws[(size_t)G + i];
+    const int ph = (int)(x >> 56);
+    lh[ph & 127]++;
+    if (ph != 99 && ph != 10 && shown < 24) {
+      fprintf(stderr, "[mlmq debug]   warp %d phase %d l0size %llu n1 %llu n2 %llu outn %llu\n", i, ph,
+              (x >> 40) & 0xFFFF, (x >> 24) & 0xFFFF, (x >> 12) & 0xFFF, x & 0xFFF);
+      ++shown;
+    }
+  }
+  fprintf(stderr, "[mlmq debug]   manager iters %llu d %llu r %llu state %llu audit %llu | ctl done %llu stop %llu err %llu epoch %llu hubwp %llu hubrp %llu idle %llu | ring0 wp %llu rp %llu | diag %llu %llu %llu %llu\n",
+          ws[2 * (size_t)G], ws[2 * (size_t)G + 2], ws[2 * (size_t)G + 3], ws[2 * (size_t)G + 4], ws[2 * (size_t)G + 5],
+          ctl[C_DONE], ctl[C_STOP], ctl[C_ERR], ctl[C_EPOCH], ctl[C_HUB_WP], ctl[C_HUB_RP], ctl[C_IDLE], ptr[0], ptr[16], ctl[C_DIAG], ctl[C_DIAG + 1], ctl[C_DIAG + 2], ctl[C_DIAG + 3]);
+  {
+    int shown2 = 0;
+    for (int i = 0; i < G && shown2 < 8; ++i) {
+      const unsigned long long* L = &ws[(size_t)2 * G + 8 + (size_t)i * 32];
+      bool same = true;
+      for (int l = 1; l < 32; ++l) same &= L[l] == L[0];
+      const bool stuck = ((ws[(size_t)G + i] >> 56) != 99);
+      if (!same || stuck) {
+        fprintf(stderr, "[mlmq debug]   warp %d lanes:", i);
+        for (int l = 0; l < 32; ++l) fprintf(stderr, " %llu", L[l]);
+        fprintf(stderr, "\n");
+        ++shown2;
+      }
+    }
+  }
+  fprintf(stderr, "[mlmq debug]   phases:");
+  for (int i = 0; i < 128; ++i)
+    if (lh[i]) fprintf(stderr, " %d:%d", i, lh[i]);
+  fprintf(stderr, "\n");
 }
 
 // One attempt at a given distance kind.  Returns MLMQ_OK, an error, or 100 when the
@@ -365,12 +418,12 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     cudaFree(g->d_prof);
     cudaFree(g->d_wstate);
     CK(cudaMalloc(&g->d_prof, (size_t)G * P_COUNT * 8));
-    CK(cudaMalloc(&g->d_wstate, (size_t)G * 8));
+    CK(cudaMalloc(&g->d_wstate, (size_t)G * 16 + 64 + (size_t)G * 256));
     g->prof_cap = G;
   }
   if (dbg) {
     CK(cudaMemset(g->d_prof, 0, (size_t)G * P_COUNT * 8));
-    CK(cudaMemset(g->d_wstate, 0, (size_t)G * 8));
+    CK(cudaMemset(g->d_wstate, 0, (size_t)G * 16 + 64 + (size_t)G * 256));
   }
   KParams p;
   std::memset(&p, 0, sizeof(p));
