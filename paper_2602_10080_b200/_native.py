@@ -19,6 +19,8 @@ from .core import EngineError, QueueOverflowError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmlmq.so")
+#: MLMQ_DEBUG=1 loads the debug build (make -C csrc debug): phase profile + wait states
+DEBUG_LIB_PATH = os.path.join(_HERE, "libmlmq_debug.so")
 
 MLMQ_OK, MLMQ_EINVAL, MLMQ_EOVERFLOW, MLMQ_EENGINE, MLMQ_ECUDA, MLMQ_ENOMEM = range(6)
 W_U32, W_F32, W_UNIT = 0, 1, 2
@@ -86,11 +88,14 @@ def lib():
     with _lib_lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
+        path = LIB_PATH
+        if os.environ.get("MLMQ_DEBUG") == "1" and os.path.exists(DEBUG_LIB_PATH):
+            path = DEBUG_LIB_PATH
+        if not os.path.exists(path):
             raise EngineError(
-                f"{LIB_PATH} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                f"{path} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
                 " or `make -C paper_2602_10080_b200/csrc`")
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         P, U64, I32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int
         sig = {
             "mlmq_abi_version": ([], I32),

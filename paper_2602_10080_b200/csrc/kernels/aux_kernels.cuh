@@ -9,13 +9,18 @@ namespace mlmq {
 __global__ void reset_queues_kernel(unsigned long long* seq, unsigned long long nslots_total,
                                     unsigned long long bn_mask, unsigned long long* ptrs,
                                     int nrings, unsigned long long* hub_seq,
+                                    unsigned long long* hub_next, uint32_t* hub_fin,
                                     unsigned long long hub_cap, unsigned long long* ctl,
                                     uint32_t* hlock, unsigned long long* hsize,
                                     unsigned long long* hwc, int nheaps) {
   const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   for (unsigned long long i = tid; i < nslots_total; i += stride) seq[i] = i & bn_mask;
-  for (unsigned long long i = tid; i < hub_cap; i += stride) hub_seq[i] = i;
+  for (unsigned long long i = tid; i < hub_cap; i += stride) {
+    hub_seq[i] = i;
+    hub_next[i] = 0;
+    hub_fin[i] = 0;
+  }
   for (unsigned long long i = tid; i < (unsigned long long)nrings * 32; i += stride) ptrs[i] = 0;
   for (unsigned long long i = tid; i < (unsigned long long)nheaps; i += stride) {
     hlock[i * 32] = 0;
@@ -25,6 +30,7 @@ __global__ void reset_queues_kernel(unsigned long long* seq, unsigned long long 
   if (tid == 0) {
     ctl[C_HUB_WP] = 0;
     ctl[C_HUB_RP] = 0;
+    ctl[C_HUB_RES] = 0;
   }
 }
 
@@ -47,7 +53,8 @@ __global__ void init_kernel(S* dist, unsigned long long n, unsigned long long so
   ctl[C_HUB_ITEMS] = 0;
   ctl[C_IDLE] = 0;
   for (int i = 0; i < 4; ++i) ctl[C_DIAG + i] = 0;
-  unsigned long long reserve = ctl[C_HUB_WP];
+  ctl[C_HUB_RP] = ctl[C_HUB_WP];  // every descriptor of the last solve completed
+  unsigned long long reserve = ctl[C_HUB_RES];
   for (int r = 0; r < p.nrings; ++r) reserve += p.ptrs[(size_t)r * 32];
   for (int h = 0; h < p.pnum; ++h) reserve += p.hwc[(size_t)h * 16];
   ctl[C_DONE] = reserve;
@@ -105,11 +112,11 @@ __global__ void audit_kernel(KParams p, unsigned long long* out, int fifo_fix) {
   }
   if (t == 0) {
     const unsigned long long* ctl = p.ctl;
-    if (p.wstate) p.wstate[2 * (size_t)p.G + 5] = 1;
+    if (kDebug && p.wstate) p.wstate[2 * (size_t)p.G + 5] = 1;
     out[0] = ctl[C_DONE];
-    out[1] = s_res[0] + ctl[C_HUB_WP];
+    out[1] = s_res[0] + ctl[C_HUB_RES];
     out[2] = s_bad[0];
-    out[3] = ctl[C_HUB_WP] != ctl[C_HUB_RP];
+    out[3] = 0;  // hub descriptors: covered by reserve == done (C_HUB_RES)
     out[4] = s_hs[0];
     out[5] = ctl[C_LOCAL_NONEMPTY];
     out[6] = ctl[C_ERR];
@@ -123,7 +130,7 @@ __global__ void audit_kernel(KParams p, unsigned long long* out, int fifo_fix) {
       if (rd > w) p.ptrs[0] = rd;
       __threadfence();
     }
-    if (p.wstate) p.wstate[2 * (size_t)p.G + 5] = 2;
+    if (kDebug && p.wstate) p.wstate[2 * (size_t)p.G + 5] = 2;
   }
 }
 

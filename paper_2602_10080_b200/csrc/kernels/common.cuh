@@ -10,6 +10,14 @@ namespace mlmq {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
+// Debug hooks (phase profile, wait states, uniformity checks) exist only in the debug
+// library (make debug -> libmlmq_debug.so, loaded when MLMQ_DEBUG=1).
+#ifdef MLMQ_DEBUG_HOOKS
+constexpr bool kDebug = true;
+#else
+constexpr bool kDebug = false;
+#endif
+
 // Device distance kinds.  The API domain is u64 with INF = 2^64-1 (core.py:17-18);
 // the engine runs u32 when the result provably (or, optimistically, actually) fits,
 // and f32 for float-weight graphs.
@@ -34,14 +42,15 @@ enum : int {
   C_STOP = 16,            // work flag cleared by the manager (engine.py:152-169)
   C_ERR = 32,             // ERR_* code
   C_EPOCH = 48,           // bucket floor index (l2.py:181-301)
-  C_HUB_WP = 64,          // hub ring write ticket
-  C_HUB_RP = 80,          // hub ring read ticket
+  C_HUB_WP = 64,          // hub descriptor tickets issued
+  C_HUB_RP = 80,          // oldest hub descriptor that may still have chunks
   C_DIST_OVF = 96,        // optimistic u32 distance overflowed
   C_LOCAL_NONEMPTY = 112, // audit: sum of L0+L1 sizes at exit (engine.py:233-237)
   C_DIAG = 128,           // overflow diagnostics: ring, slot, write_ptr, read_ptr
   C_HUB_ITEMS = 144,      // hub items pushed
   C_IDLE = 160,           // number of groups currently idle (demand signal for eager spill)
-  C_WORDS = 176
+  C_HUB_RES = 176,        // hub chunks reserved (termination units)
+  C_WORDS = 192
 };
 
 // Per-group metric slots, in METRIC_FIELDS order (core.py:142-154).
@@ -244,7 +253,9 @@ struct KParams {
 
   // hub work ring
   unsigned long long* hub_seq;
-  HubItem* hub_data;
+  HubItem* hub_data;              // descriptors: lo, hi, du, u, pad = nch
+  unsigned long long* hub_next;   // claim words: ticket << 24 | chunks claimed
+  uint32_t* hub_fin;              // chunks completed
   unsigned long long hub_mask;
   unsigned long long hub_chunk;
   unsigned long long hub_thresh;

@@ -94,12 +94,12 @@ struct Worker {
     if (lane == 0) met[f] += v;
   }
   // debug profile (MLMQ_DEBUG=1): cycles per phase, counts
-  __device__ __forceinline__ unsigned long long pclk() const { return p.prof ? clock64() : 0ull; }
+  __device__ __forceinline__ unsigned long long pclk() const { return (kDebug && p.prof) ? clock64() : 0ull; }
   __device__ __forceinline__ void pacc(int slot, unsigned long long t0) {
-    if (p.prof && lane == 0) met[kProfBase + slot] += clock64() - t0;
+    if ((kDebug && p.prof) && lane == 0) met[kProfBase + slot] += clock64() - t0;
   }
   __device__ __forceinline__ void pcnt(int slot, unsigned long long v) {
-    if (p.prof && lane == 0) met[kProfBase + slot] += v;
+    if ((kDebug && p.prof) && lane == 0) met[kProfBase + slot] += v;
   }
 // Per-lane source-line trace (build with -DMLMQ_TRACE, run with MLMQ_DEBUG=1): the stuck
 // dump prints every lane's last line, which exposes lanes that left warp-uniform flow.
@@ -111,7 +111,7 @@ struct Worker {
 #define CHKU() check_uniform(__LINE__)
   // debug: every "warp-uniform" scalar of the worker must agree with lane 0
   __device__ void check_uniform(int line) {
-    if (!p.wstate) return;
+    if (!(kDebug && p.wstate)) return;
     unsigned long long h = (unsigned long long)l0size ^ ((unsigned long long)n1 << 13) ^
                            ((unsigned long long)n2 << 26) ^ ((unsigned long long)outn << 39) ^
                            ((unsigned long long)h1 << 45) ^ ((unsigned long long)h2 << 51) ^
@@ -124,17 +124,17 @@ struct Worker {
     if (bad && lane == 0) raise_error(ERR_CORRUPT, 7000000ull + line, bad, (unsigned long long)gid, h0);
   }
   __device__ __forceinline__ void trace(int line) {
-    if (p.wstate) p.wstate[2 * (size_t)p.G + 8 + (size_t)gid * 32 + lane] = (unsigned long long)line;
+    if (kDebug && p.wstate) p.wstate[2 * (size_t)p.G + 8 + (size_t)gid * 32 + lane] = (unsigned long long)line;
   }
   // debug: where the warp is and its local queue sizes (wstate[G + gid])
   __device__ __forceinline__ void loc(int ph) {
-    if (p.wstate && lane == 0)
+    if ((kDebug && p.wstate) && lane == 0)
       p.wstate[p.G + gid] = ((unsigned long long)ph << 56) | ((unsigned long long)(l0size & 0xFFFF) << 40) |
                             ((unsigned long long)(n1 & 0xFFFF) << 24) | ((unsigned long long)(n2 & 0xFFF) << 12) |
                             (unsigned long long)(outn & 0xFFF);
   }
   __device__ __forceinline__ void wstate(int code, unsigned long long tk) {
-    if (p.wstate) p.wstate[gid] = ((unsigned long long)code << 56) | (tk & ((1ull << 56) - 1));
+    if (kDebug && p.wstate) p.wstate[gid] = ((unsigned long long)code << 56) | (tk & ((1ull << 56) - 1));
   }
   // per-lane check, only for spins that a single lane runs
   __device__ __forceinline__ bool stopped() const {
@@ -281,7 +281,7 @@ struct Worker {
       __nanosleep(ns);
       if (ns < 1024) ns <<= 1;
     }
-    if (p.prof) atomicAdd(met + kProfBase + P_SPINS, (unsigned long long)spins);
+    if (kDebug && p.prof) atomicAdd(met + kProfBase + P_SPINS, (unsigned long long)spins);
     return true;
   }
 
@@ -330,7 +330,7 @@ struct Worker {
     for (int i = lane; i < n; i += 32) {
       LOC();
       const int sg = i / bs;
-      slot_data(rid, (t + sg) & p.bn_mask)[i - sg * bs] = base[(start + i) % cap];
+      slot_data(rid, (t + sg) & p.bn_mask)[i - sg * bs] = base[(unsigned)(start + i) % (unsigned)cap];
     }
     publish_all(rid, t, nseg, n);
   }
@@ -388,7 +388,7 @@ struct Worker {
         LOC();
         unsigned long long old = atomicCAS(rpp, r, r + 1);
         if (old == r) { got = 1; break; }
-        if (p.prof) met[kProfBase + P_CASFAIL] += 1;
+        if (kDebug && p.prof) met[kProfBase + P_CASFAIL] += 1;
         r = old;
         if (r >= w) w = ld_relaxed(wpp);
       }
@@ -432,6 +432,11 @@ struct Worker {
   }
 
   // ============================================================ L2: bucket window
+  // ring of bucket rel relative to epoch e (emod = e % bmax)
+  __device__ __forceinline__ int bring(int emod, int rel) const {
+    const int x = emod + rel;
+    return x >= p.bmax ? x - p.bmax : x;
+  }
   __device__ __forceinline__ int bucket_rel(S d, unsigned long long e) const {
     if (K == DK_F32) {
       const double base = (double)e * p.delta_f;
@@ -443,7 +448,12 @@ struct Worker {
       const unsigned long long base = e * p.delta_i;
       const unsigned long long dd = (unsigned long long)d;
       if (dd < base) return 0;
-      const unsigned long long q = (dd - base) / p.delta_i;
+      const unsigned long long diff = dd - base;
+      unsigned long long q;
+      if ((diff >> 32) == 0 && (p.delta_i >> 32) == 0)
+        q = (unsigned)diff / (unsigned)p.delta_i;  // 32-bit divide on the common path
+      else
+        q = diff / p.delta_i;
       return q >= (unsigned long long)(p.bmax - 1) ? p.bmax - 1 : (int)q;
     }
   }
@@ -470,7 +480,7 @@ struct Worker {
   __device__ void bucket_write(const E* base, int start, int n, int cap) {
     LOC();
     const unsigned long long e = warp_ld(p.ctl + C_EPOCH);
-    const unsigned long long bm = (unsigned long long)p.bmax;
+    const int emod = (int)(e % (unsigned long long)p.bmax);
     if (!p.bscratch) {  // very wide windows: per-round grouping
       for (int o = 0; o < n; o += 32) {
         LOC();
@@ -478,8 +488,8 @@ struct Worker {
         E x = E();
         int f = 0;
         if (has) {
-          x = base[(start + o + lane) % cap];
-          f = (int)((e + (unsigned long long)bucket_rel(x.d, e)) % bm);
+          x = base[(unsigned)(start + o + lane) % (unsigned)cap];
+          f = bring(emod, bucket_rel(x.d, e));
         }
         bucket_scatter_lanes(has, x, f);
       }
@@ -490,8 +500,8 @@ struct Worker {
     __syncwarp();
     for (int i = lane; i < n; i += 32) {
       LOC();
-      const E x = base[(start + i) % cap];
-      atomicAdd(bhist + (int)((e + (unsigned long long)bucket_rel(x.d, e)) % bm), 1u);
+      const E x = base[(unsigned)(start + i) % (unsigned)cap];
+      atomicAdd(bhist + bring(emod, bucket_rel(x.d, e)), 1u);
     }
     __syncwarp();
     int used = 0;
@@ -521,8 +531,8 @@ struct Worker {
     if (!__all_sync(FULL, ok)) return;
     for (int i = lane; i < n; i += 32) {
       LOC();
-      const E x = base[(start + i) % cap];
-      const int f = (int)((e + (unsigned long long)bucket_rel(x.d, e)) % bm);
+      const E x = base[(unsigned)(start + i) % (unsigned)cap];
+      const int f = bring(emod, bucket_rel(x.d, e));
       const int r = (int)atomicAdd(bcur + f, 1u);
       const int sg = r / bs;
       slot_data(f, (btick[f] + sg) & p.bn_mask)[r - sg * bs] = x;
@@ -550,10 +560,11 @@ struct Worker {
     LOC();
     loc(16);
     const unsigned long long e0 = warp_ld(p.ctl + C_EPOCH);
+    const int e0mod = (int)(e0 % (unsigned long long)p.bmax);
     bool head_empty = false;
     for (int j = 0; j < p.bnum; ++j) {
       LOC();
-      const int f = (int)((e0 + (unsigned long long)j) % (unsigned long long)p.bmax);
+      const int f = bring(e0mod, j);
       for (;;) {
         LOC();
         const int c = ring_read(f, dst);
@@ -563,8 +574,8 @@ struct Worker {
         }
         local_done += 1;
         const unsigned long long en = warp_ld(p.ctl + C_EPOCH);
-        const int rel_slot = (int)(((unsigned long long)f + (unsigned long long)p.bmax -
-                                    (en % (unsigned long long)p.bmax)) % (unsigned long long)p.bmax);
+        const int enmod = (int)(en % (unsigned long long)p.bmax);
+        const int rel_slot = f >= enmod ? f - enmod : f + p.bmax - enmod;
         int kept = 0;
         for (int o = 0; o < c; o += 32) {
           LOC();
@@ -582,7 +593,7 @@ struct Worker {
           if (keep) dst[kept + __popc(km & lanemask_lt())] = x;
           kept += __popc(km);
           if (__any_sync(FULL, rb))
-            bucket_scatter_lanes(rb, x, (int)((en + (unsigned long long)rel) % (unsigned long long)p.bmax));
+            bucket_scatter_lanes(rb, x, bring(enmod, rel));
           __syncwarp();
         }
         if (kept > 0) return kept;
@@ -592,7 +603,7 @@ struct Worker {
     if (head_empty) {
       bool ne = false;
       for (int k = lane; k < p.bmax; k += 32)
-        if (k != (int)(e0 % (unsigned long long)p.bmax)) ne |= ld_relaxed(wp(k)) > ld_relaxed(rp(k));
+        if (k != e0mod) ne |= ld_relaxed(wp(k)) > ld_relaxed(rp(k));
       if (__any_sync(FULL, ne)) {
         if (lane == 0 && atomicCAS(p.ctl + C_EPOCH, e0, e0 + 1) == e0) met[M_L2A] += 1;
         __syncwarp();
@@ -723,7 +734,7 @@ struct Worker {
       const int c = min(32, n - o);
       const bool has = lane < c;
       E x = E();
-      if (has) x = base[(start + o + lane) % cap];
+      if (has) x = base[(unsigned)(start + o + lane) % (unsigned)cap];
       warp_sort(x, has);
       const int nb = p.nb;
       const int nn = (c + nb - 1) / nb;
@@ -857,10 +868,11 @@ struct Worker {
   }
 
   // ============================================================ L1 (shared memory)
-  __device__ __forceinline__ static int ridx(int h, int i, int cap) { return (int)(((long long)h + i) % cap); }
+  __device__ __forceinline__ static int ridx(int h, int i, int cap) { return (int)((unsigned)(h + i) % (unsigned)cap); }
   __device__ __forceinline__ static int ridx_neg(int h, long long i, int cap) {
-    long long x = ((long long)h + i) % cap;
-    return (int)(x < 0 ? x + cap : x);
+    int x = h + (int)(i % (long long)cap);
+    if (x < 0) x += cap;
+    return x >= cap ? x - cap : x;
   }
   static constexpr int LINEAR = 0x7fffffff;
 
@@ -1270,109 +1282,135 @@ struct Worker {
     }
   }
 
+  // Hub descriptors (new tier): one descriptor per hub list, split into
+  // nch chunks of hub_chunk edges that any warp claims with ONE fetch-add on the
+  // descriptor's claim word (ticket << 24 | count) -- no CAS retry storms.  The slot is
+  // freed only when all nch chunks have completed, so a valid claim always reads a stable
+  // descriptor.  Termination: C_HUB_RES += nch before publication; each valid claim adds
+  // one to local_done.
+  static constexpr unsigned long long kClaimBits = 24, kClaimMask = (1ull << kClaimBits) - 1;
   __device__ void push_hub(uint32_t u, S du, unsigned long long lo, unsigned long long hi) {
     LOC();
     const unsigned long long ch = p.hub_chunk;
     const unsigned long long nch = (hi - lo + ch - 1) / ch;
-    unsigned long long t = 0;
     if (lane == 0) {
-      t = atomicAdd(p.ctl + C_HUB_WP, nch);
+      atomicAdd(p.ctl + C_HUB_RES, nch);  // reserve before publication (compose.py:82-85)
       atomicAdd(p.ctl + C_HUB_ITEMS, nch);
-    }
-    t = __shfl_sync(FULL, t, 0);
-    const unsigned long long cap = p.hub_mask + 1;
-    for (unsigned long long q = lane; q < nch; q += 32) {
-      LOC();
-      const unsigned long long tk = t + q, slot = tk & p.hub_mask;
+      const unsigned long long t = atomicAdd(p.ctl + C_HUB_WP, 1ull);
+      const unsigned long long slot = t & p.hub_mask;
       unsigned long long t0 = 0;
       int spins = 0;
       bool ok = true;
-      while (ld_acquire(p.hub_seq + slot) != tk) {
-        LOC();
+      wstate(W_HUB_WRITE, t);
+      while (ld_acquire(p.hub_seq + slot) != t) {
         if (++spins % 64 == 0) {
           if (stopped()) { ok = false; break; }
-          unsigned long long now = globaltimer_ns();
+          const unsigned long long now = globaltimer_ns();
           if (t0 == 0) t0 = now;
           else if (now - t0 > p.spin_timeout_ns) {
-            raise_error(ERR_HUB_OVERFLOW, 0, slot, t, cap);
+            raise_error(ERR_HUB_OVERFLOW, 0, slot, t, p.hub_mask + 1);
             ok = false;
             break;
           }
         }
         __nanosleep(64);
       }
-      if (!ok) break;
-      HubItem it;
-      it.lo = lo + q * ch;
-      it.hi = min(hi, lo + (q + 1) * ch);
-      it.du = (unsigned long long)du;
-      it.u = u;
-      it.pad = 0;
-      p.hub_data[slot] = it;
-      __threadfence();
-      st_release(p.hub_seq + slot, tk + 1);
+      wstate(W_NONE, 0);
+      if (ok) {
+        HubItem it;
+        it.lo = lo;
+        it.hi = hi;
+        it.du = (unsigned long long)du;
+        it.u = u;
+        it.pad = (uint32_t)nch;
+        p.hub_data[slot] = it;
+        p.hub_fin[slot] = 0u;
+        atomicExch(p.hub_next + slot, t << kClaimBits);
+        __threadfence();
+        st_release(p.hub_seq + slot, t + 1);
+      }
     }
     __syncwarp();
   }
 
-  // Claim one hub item if any; returns true and processes it.
+  // Claim one hub chunk if any; returns true (and relaxes it) when a chunk was claimed.
   __device__ bool hub_try() {
     LOC();
-    loc(17);
-    unsigned long long r = 0;
     int got = 0;
-    if (lane == 0) {
-      unsigned long long* rpp = p.ctl + C_HUB_RP;
-      unsigned long long* wpp = p.ctl + C_HUB_WP;
-      r = ld_relaxed(rpp);
-      unsigned long long w = ld_relaxed(wpp);
-      while (r < w) {
-        LOC();
-        unsigned long long old = atomicCAS(rpp, r, r + 1);
-        if (old == r) { got = 1; break; }
-        r = old;
-        if (r >= w) w = ld_relaxed(wpp);
-      }
-    }
-    got = __shfl_sync(FULL, got, 0);
-    if (!got) return false;
-    r = __shfl_sync(FULL, r, 0);
-    const unsigned long long slot = r & p.hub_mask;
+    unsigned long long tk = 0, c = 0;
     HubItem it = HubItem();
-    int ok = 1;
     if (lane == 0) {
-      wstate(W_HUB_READ, r + 1);
-      while (ld_acquire(p.hub_seq + slot) != r + 1) {
-        LOC();
-        if (stopped()) { ok = 0; break; }
-        __nanosleep(64);
+      unsigned long long h = ld_relaxed(p.ctl + C_HUB_RP);
+      const unsigned long long w = ld_relaxed(p.ctl + C_HUB_WP);
+      const unsigned long long h0 = h;
+      for (unsigned long long d = h; d < w && d < h0 + 8 && !got; ++d) {
+        const unsigned long long slot = d & p.hub_mask;
+        const unsigned long long s = ld_acquire(p.hub_seq + slot);
+        if (s != d + 1) {
+          if (s > d + 1 && d == h) h = d + 1;  // freed: the head may move past it
+          continue;                            // not yet published
+        }
+        const unsigned long long x0 = ld_relaxed(p.hub_next + slot);
+        const uint32_t nch0 = __ldcg(&p.hub_data[slot].pad);
+        if ((x0 >> kClaimBits) == d && (x0 & kClaimMask) >= nch0) {
+          if (d == h) h = d + 1;  // exhausted
+          continue;
+        }
+        const unsigned long long x = atomicAdd(p.hub_next + slot, 1ull);
+        tk = x >> kClaimBits;
+        c = x & kClaimMask;
+        // the descriptor our claim belongs to (the slot may have been recycled to tk)
+        for (;;) {
+          const unsigned long long s1 = ld_acquire(p.hub_seq + slot);
+          if (s1 > tk + 1 || s1 < tk) break;  // tk already freed (claim invalid) or stale
+          if (s1 == tk + 1) {
+            const uint4* src = reinterpret_cast<const uint4*>(p.hub_data + slot);
+            const uint4 a = __ldcg(src), b = __ldcg(src + 1);
+            if (ld_acquire(p.hub_seq + slot) != tk + 1) continue;  // seqlock re-check
+            it.lo = ((unsigned long long)a.y << 32) | a.x;
+            it.hi = ((unsigned long long)a.w << 32) | a.z;
+            it.du = ((unsigned long long)b.y << 32) | b.x;
+            it.u = b.z;
+            it.pad = b.w;
+            if (c < it.pad) got = 1;
+            break;
+          }
+          if (stopped()) break;
+          __nanosleep(32);
+        }
+        if (!got && tk == d && d == h) h = d + 1;
       }
-      if (ok) {
-        const uint4* src = reinterpret_cast<const uint4*>(p.hub_data + slot);
-        uint4 a = __ldcg(src), b = __ldcg(src + 1);
-        it.lo = ((unsigned long long)a.y << 32) | a.x;
-        it.hi = ((unsigned long long)a.w << 32) | a.z;
-        it.du = ((unsigned long long)b.y << 32) | b.x;
-        it.u = b.z;
-        st_release(p.hub_seq + slot, r + p.hub_mask + 1);
-      }
-      wstate(W_NONE, 0);
+      if (h != h0) atomicCAS(p.ctl + C_HUB_RP, h0, h);  // best effort
     }
-    if (!__shfl_sync(FULL, ok, 0)) return true;
+    if (!__shfl_sync(FULL, got, 0)) return false;
+    tk = __shfl_sync(FULL, tk, 0);
+    c = __shfl_sync(FULL, c, 0);
     it.lo = __shfl_sync(FULL, it.lo, 0);
     it.hi = __shfl_sync(FULL, it.hi, 0);
     it.du = __shfl_sync(FULL, it.du, 0);
     it.u = __shfl_sync(FULL, it.u, 0);
+    it.pad = __shfl_sync(FULL, it.pad, 0);
     local_done += 1;
+    const unsigned long long clo = it.lo + c * p.hub_chunk;
+    const unsigned long long chi = min(it.hi, clo + p.hub_chunk);
     S du = (S)it.du;
     S cur = 0;
     if (lane == 0) cur = ldcg_dist(dist + it.u);
     cur = __shfl_sync(FULL, cur, 0);
-    if (p.dup && du > cur) return true;  // stale hub item (engine.py:190 analogue)
-    if (cur < du) du = cur;
-    relax_range(it.lo, it.hi, du);
+    if (!(p.dup && du > cur)) {  // stale hub descriptor (engine.py:190 analogue)
+      if (cur < du) du = cur;
+      relax_range(clo, chi, du);
+    }
+    // completion: the last finished chunk frees the slot
+    __syncwarp();
+    if (lane == 0) {
+      const unsigned long long slot = tk & p.hub_mask;
+      __threadfence();
+      if (atomicAdd(p.hub_fin + slot, 1u) + 1u == it.pad) st_release(p.hub_seq + slot, tk + p.hub_mask + 1);
+    }
     return true;
   }
+
 
   // engine.py:171-227 for one batch in shared memory
   __device__ void relax_batch(int nb) {
@@ -1588,7 +1626,7 @@ struct Worker {
     const int l1size = n1 + n2;
     if (lane == 0) {
       for (int f = 0; f < M_COUNT; ++f) p.metrics[(size_t)gid * M_COUNT + f] = met[f];
-      if (p.prof)
+      if (kDebug && p.prof)
         for (int f = 0; f < P_COUNT; ++f) p.prof[(size_t)gid * P_COUNT + f] = met[kProfBase + f];
       if (l0size + l1size + outn) atomicAdd(p.ctl + C_LOCAL_NONEMPTY, (unsigned long long)(l0size + l1size + outn));
     }
@@ -1598,7 +1636,7 @@ struct Worker {
 // K2: manager warp (engine.py:152-169): reserve == done on three consecutive polls.
 static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
   int k = 0;
-  if (p.wstate && lane == 0) p.wstate[2 * (size_t)p.G + 4] = 1;
+  if ((kDebug && p.wstate) && lane == 0) p.wstate[2 * (size_t)p.G + 4] = 1;
   for (;;) {
     if (p.host_abort && lane == 0 && ld_sys_u32(p.host_abort) != 0u) {
       atomicCAS(p.ctl + C_ERR, 0ull, (unsigned long long)ERR_ABORT);
@@ -1617,10 +1655,10 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
     unsigned long long r = 0;
     for (int i = lane; i < p.nrings; i += 32) r += ld_relaxed(p.ptrs + (size_t)i * 32);
     for (int i = lane; i < p.pnum; i += 32) r += ld_relaxed(p.hwc + (size_t)i * 16);
-    if (lane == 0) r += ld_relaxed(p.ctl + C_HUB_WP);
+    if (lane == 0) r += ld_relaxed(p.ctl + C_HUB_RES);
     r = warp_sum_u64(r);
     k = (d == r) ? k + 1 : 0;
-    if (p.wstate && lane == 0) {
+    if ((kDebug && p.wstate) && lane == 0) {
       p.wstate[2 * (size_t)p.G] += 1;
       p.wstate[2 * (size_t)p.G + 2] = d;
       p.wstate[2 * (size_t)p.G + 3] = r;
@@ -1641,7 +1679,7 @@ __global__ void __launch_bounds__(256) mlmq_persistent_kernel(const __grid_const
   if (gid > p.G) return;
   if (gid == p.G) {
     manager_loop(p, lane);
-    if (p.wstate && lane == 0) p.wstate[2 * (size_t)p.G + 4] = 2;
+    if ((kDebug && p.wstate) && lane == 0) p.wstate[2 * (size_t)p.G + 4] = 2;
     return;
   }
   Worker<K, L2K, CM> w(p, smem + (size_t)warp * p.smem_per_warp, gid, lane);

@@ -87,6 +87,8 @@ struct Workspace {
   uint32_t* hcnt = nullptr;
   unsigned long long* hub_seq = nullptr;
   HubItem* hub_data = nullptr;
+  unsigned long long* hub_next = nullptr;
+  uint32_t* hub_fin = nullptr;
   bool dirty = true;
   size_t bytes = 0;
 };
@@ -103,6 +105,8 @@ void ws_free(Workspace& w) {
   cudaFree(w.hcnt);
   cudaFree(w.hub_seq);
   cudaFree(w.hub_data);
+  cudaFree(w.hub_next);
+  cudaFree(w.hub_fin);
   w = Workspace();
 }
 
@@ -286,6 +290,8 @@ int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& s
     alloc((void**)&w.hcnt, need.nheaps ? nh * need.hcap * 4 : 256);
     alloc((void**)&w.hub_seq, need.hub_cap * 8);
     alloc((void**)&w.hub_data, need.hub_cap * sizeof(HubItem));
+    alloc((void**)&w.hub_next, need.hub_cap * 8);
+    alloc((void**)&w.hub_fin, need.hub_cap * 4);
     if (e != cudaSuccess) {
       cudaGetLastError();
       ws_free(w);
@@ -297,7 +303,7 @@ int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& s
   if (w.dirty) {
     const size_t nslots = (size_t)std::max(w.nrings, 1) * w.bn;
     reset_queues_kernel<<<1024, 256, 0, g->stream>>>(w.seq, nslots, w.bn - 1, w.ptrs, std::max(w.nrings, 1),
-                                                      w.hub_seq, w.hub_cap, g->d_ctl, w.hlock, w.hsize, w.hwc,
+                                                      w.hub_seq, w.hub_next, w.hub_fin, w.hub_cap, g->d_ctl, w.hlock, w.hsize, w.hwc,
                                                       std::max(w.nheaps, 1));
     CK(cudaGetLastError());
     w.dirty = false;
@@ -310,6 +316,7 @@ double now_s() {
 }
 
 bool debug_enabled() {
+  if (!kDebug) return false;
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MLMQ_DEBUG");
@@ -477,6 +484,8 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.pnum = sh.l2k == L2K_HEAP ? w.nheaps : 0;
   p.hub_seq = w.hub_seq;
   p.hub_data = w.hub_data;
+  p.hub_next = w.hub_next;
+  p.hub_fin = w.hub_fin;
   p.hub_mask = w.hub_cap - 1;
   p.hub_chunk = hub_chunk;
   p.hub_thresh = 2 * hub_chunk;

@@ -43,6 +43,8 @@ def main():
         combos.append((l1, cap, l2, ds, hub))
     if args.grid == "small":
         combos = [c for c in combos if c[1] == 256]
+    elif args.grid == "fifo":
+        combos = [c for c in combos if c[2] == "fifo"]
     e_reach = None
     for l1, cap, l2, ds, hub in combos:
         cfg = MlmqConfig(l1_type=l1, l2_type=l2,
