@@ -184,6 +184,14 @@ __device__ __forceinline__ Elem<unsigned long long> ld_cg_elem(const Elem<unsign
 __device__ __forceinline__ uint32_t ldcg_dist(const uint32_t* p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned long long ldcg_dist(const unsigned long long* p) { return __ldcg(p); }
 
+// atomic min without a return value (RED.MIN at L2)
+__device__ __forceinline__ void red_min(uint32_t* a, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_min(unsigned long long* a, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -25,7 +25,7 @@ struct Worker {
   using Tr = DT<K>;
   using S = typename Tr::S;
   using E = Elem<S>;
-  static constexpr int U = 4;  // edge slots per lane per step
+  static constexpr int U = 8;  // edge slots per lane per step (8 independent loads in flight)
 
   const KParams& p;
   S* dist;
@@ -53,6 +53,7 @@ struct Worker {
   int wcount;
 
   unsigned long long local_done;
+  unsigned n_relax, n_upd;  // relaxations (per lane) / distance updates (warp), folded at exit
   int mcursor;
   int outn;
   bool dist_ovf;
@@ -82,6 +83,7 @@ struct Worker {
     has_rej = false;
     wcount = 0;
     local_done = 0;
+    n_relax = n_upd = 0;
     mcursor = p.pnum > 0 ? gid % p.pnum : 0;
     outn = 0;
     dist_ovf = false;
@@ -1219,12 +1221,13 @@ struct Worker {
   // improves (core.py:205-213): emit (v, nd).
   __device__ void relax_slots(bool (&act)[U], const unsigned long long (&kk)[U], const S (&du)[U]) {
     LOC();
-    uint32_t v[U] = {0, 0, 0, 0};
-    S nd[U] = {0, 0, 0, 0};
+    uint32_t v[U];
+    S nd[U];
     int c = 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      LOC();
+      v[j] = 0;
+      nd[j] = 0;
       if (act[j]) {
         const uint2 a = __ldg(p.adj + kk[j]);
         v[j] = a.x;
@@ -1236,18 +1239,17 @@ struct Worker {
 #pragma unroll
     for (int j = 0; j < U; ++j)
       if (act[j]) act[j] = nd[j] < ldcg_dist(dist + v[j]);
+    // Fire-and-forget atomic min (RED, no round trip): an edge whose prefilter saw an
+    // improvement enqueues (v, nd) whether or not its RED ends up the minimum.  The
+    // writer of the final dist[v] always passed its prefilter, so v is expanded with
+    // its final distance; a concurrently beaten element is a stale duplicate that the
+    // dequeue-side check (engine.py:190-191) drops.
 #pragma unroll
     for (int j = 0; j < U; ++j)
-      if (act[j]) act[j] = nd[j] < atomicMin(dist + v[j], nd[j]);
-    const int tot = __reduce_add_sync(FULL, c);
-    if (outn < 0 || outn >= L) {
-      if (lane == 0) raise_error(ERR_CORRUPT, 20, (unsigned long long)outn, (unsigned long long)gid, 0);
-      outn = 0;
-    }
+      if (act[j]) red_min(dist + v[j], nd[j]);
     int upd = 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      LOC();
       const unsigned m = __ballot_sync(FULL, act[j]);
       if (act[j]) {
         E e;
@@ -1258,8 +1260,8 @@ struct Worker {
       outn += __popc(m);
       upd += __popc(m);
     }
-    count(M_RELAX, (unsigned long long)tot);
-    count(M_UPD, (unsigned long long)upd);
+    n_relax += (unsigned)c;  // per lane; folded at exit
+    n_upd += (unsigned)upd;  // warp total, lane-replicated
     __syncwarp();
     if (outn >= L) flush_out(false);
   }
@@ -1267,7 +1269,9 @@ struct Worker {
   // the whole warp strides one edge list (engine.py:212-220 "big" tier, hub chunks)
   __device__ void relax_range(unsigned long long lo, unsigned long long hi, S du) {
     LOC();
-    const S dus[U] = {du, du, du, du};
+    S dus[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) dus[j] = du;
     for (unsigned long long k0 = lo; k0 < hi; k0 += 32 * U) {
       LOC();
       bool act[U];
@@ -1435,17 +1439,19 @@ struct Worker {
           valid = false;
         }
       }
-      if (valid) {
-        const S cur = ldcg_dist(dist + e.v);
-        if (p.dup && e.d > cur) valid = false;  // stale duplicate (engine.py:190-191)
-        du = e.d < cur ? e.d : cur;
-      }
-      const unsigned vm = __ballot_sync(FULL, valid);
-      count(M_SETTLED, (unsigned long long)__popc(vm));
-      if (valid) {
+      S cur = (S)Tr::INF;
+      if (valid) {  // dist[u] and the row offsets are independent loads: issue together
+        cur = ldcg_dist(dist + e.v);
         lo = __ldg(p.off + e.v);
         hi = __ldg(p.off + e.v + 1);
       }
+      if (valid) {
+        if (p.dup && e.d > cur) valid = false;  // stale duplicate (engine.py:190-191)
+        du = e.d < cur ? e.d : cur;
+      }
+      if (!valid) lo = hi = 0;
+      const unsigned vm = __ballot_sync(FULL, valid);
+      count(M_SETTLED, (unsigned long long)__popc(vm));
       // hub tier: split huge lists into shared edge-range items
       unsigned hm = __ballot_sync(FULL, valid && (hi - lo) > p.hub_thresh);
       while (hm) {
@@ -1459,11 +1465,12 @@ struct Worker {
         if (lane == l) hi = lo + p.hub_chunk;
         hm &= hm - 1;
       }
-      const unsigned long long deg = hi - lo;
-      const bool big = valid && deg > (unsigned long long)p.th_v;
-      const bool small = valid && !big;
-      // small lists: flattened, load-balanced across lanes (warp scan + search)
-      const int ds = small ? (int)deg : 0;
+      // Every list up to the hub threshold is flattened across the warp (warp scan +
+      // shuffle search), so lists of any length keep all 32 x U edge slots busy.  The
+      // reference's th_v split (engine.py:195-220) only orders the same edge set; the
+      // relaxed edges and the metrics are identical, and on the GPU one load-balanced
+      // pass beats a warp-wide walk per list above th_v.
+      const int ds = (int)(hi - lo);
       const int incl = warp_incl_scan(ds, lane);
       const int total = __shfl_sync(FULL, incl, 31);
       const int excl = incl - ds;
@@ -1490,14 +1497,6 @@ struct Worker {
           kk[j] = olo + (unsigned long long)(idx - oex);
         }
         relax_slots(act, kk, dus);
-      }
-      // big lists: the whole warp walks each one
-      unsigned bm = __ballot_sync(FULL, big);
-      while (bm) {
-        LOC();
-        const int l = __ffs(bm) - 1;
-        relax_range(__shfl_sync(FULL, lo, l), __shfl_sync(FULL, hi, l), __shfl_sync(FULL, du, l));
-        bm &= bm - 1;
       }
     }
     flush_out(true);
@@ -1570,9 +1569,14 @@ struct Worker {
     LOC();
     int backoff = 0;
     const unsigned long long tstart = pclk();
+    int since_check = 0;
     for (;;) {
       LOC();
-      if (stopped_warp()) break;
+      // a busy warp polls the stop word every 16 iterations; an idle one every time
+      if ((idle || ++since_check >= 16)) {
+        since_check = 0;
+        if (stopped_warp()) break;
+      }
       CHKU();
       loc(10);
       const int c = read_cascade();
@@ -1624,6 +1628,14 @@ struct Worker {
     // exit: metric shard + audit evidence
     if (__any_sync(FULL, dist_ovf) && lane == 0) atomicOr(p.ctl + C_DIST_OVF, 1ull);
     const int l1size = n1 + n2;
+    {
+      const unsigned long long rl = warp_sum_u64((unsigned long long)n_relax);
+      if (lane == 0) {
+        met[M_RELAX] += rl;
+        met[M_UPD] += (unsigned long long)n_upd;
+      }
+      __syncwarp();
+    }
     if (lane == 0) {
       for (int f = 0; f < M_COUNT; ++f) p.metrics[(size_t)gid * M_COUNT + f] = met[f];
       if (kDebug && p.prof)

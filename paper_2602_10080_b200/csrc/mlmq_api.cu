@@ -70,7 +70,7 @@ using namespace mlmq;
 namespace {
 
 constexpr int kWarpsPerBlockMax = 8;
-constexpr int kOutCap = 32 * 4 + 32;
+constexpr int kOutCap = 32 * 8 + 32;  // L - 1 carried + 32 lanes x U=8 winners
 constexpr int kAuditWords = 14;
 
 struct Workspace {
@@ -410,7 +410,7 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     set_last_error("num_groups=%d exceeds the %d groups the device keeps resident for this configuration", G, sh.max_groups);
     return MLMQ_EINVAL;
   }
-  const unsigned long long hub_chunk = c->hub_chunk > 0 ? (unsigned long long)c->hub_chunk : 2048ull;
+  const unsigned long long hub_chunk = c->hub_chunk > 0 ? std::min<unsigned long long>((unsigned long long)c->hub_chunk, 1ull << 20) : 3072ull;
   if ((st = ensure_workspace(g, c, sh, hub_chunk))) return st;
   if (g->metrics_cap < (unsigned long long)G) {
     cudaFree(g->d_metrics);

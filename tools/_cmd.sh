@@ -1,8 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for c in vector+fifo "vector+bucket(d4)" near_far+fifo "near_far+bucket(d1)" filter+fifo "filter+bucket(d4)" slf+fifo "slf+bucket(d1)"; do
-  l1=${c%%+*}; l2=${c#*+}
-  timeout 60 python tools/repro.py rmat 16 $l1 "$l2" 10 1024 auto > gpurun_out/r9.log 2>&1 || { echo "FAIL $c rc=$?" >> gpurun_out/repro9.log; grep -A5 "EXC" gpurun_out/r9.log | cut -c1-300 >> gpurun_out/repro9.log; }
-  echo "$c ok=$(grep -c True gpurun_out/r9.log) false=$(grep -c False gpurun_out/r9.log)" >> gpurun_out/repro9.log
-done
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
-timeout 600 python tools/tune.py --config c2 --grid fifo > gpurun_out/tune_c2_fifo2.log 2>&1
+timeout 900 python tools/sweep.py c2 'l1=vector cap=1024 l0=1,4 hub=3072,4096,6144,8192 groups=1184,auto' > gpurun_out/sweep_hub.log 2>&1
+timeout 1200 python tools/sweep.py c3 'l1=vector,filter cap=1024 l2=fifo,bucket d=1,8 reps=1' > gpurun_out/sweep_c3.log 2>&1

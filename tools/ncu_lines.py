@@ -25,3 +25,10 @@ acc.sort(reverse=True)
 print(f"total samples {tot}")
 for s, i, loc, src in acc[:top]:
     print(f"{100*s/tot:5.1f}%  inst={i:>12d}  {loc:28s} {src}")
+
+if len(sys.argv) > 3 and sys.argv[3] == "inst":
+    acc.sort(key=lambda a: -a[1])
+    ti = sum(a[1] for a in acc) or 1
+    print(f"\nby instructions executed (total {ti})")
+    for s, i, loc, src in acc[:top]:
+        print(f"{100*i/ti:5.1f}%  samples={100*s/tot:5.1f}%  {loc:28s} {src}")
