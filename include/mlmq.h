@@ -82,7 +82,9 @@ typedef struct {
   int32_t hub_chunk;                /* edges per hub work item (0 = library default)  */
   int32_t share;                    /* 1: eager L1/L0 write-back while groups are idle */
   int32_t fifo_park;                /* 1: FIFO readers take unconditional tickets      */
-  int32_t reserved[5];
+  int32_t bucket_window;            /* bucket L2: winners >= this many buckets above the
+                                       floor bypass L0/L1 (0 = reference cascade)       */
+  int32_t reserved[4];
 } mlmq_config_t;
 
 /*

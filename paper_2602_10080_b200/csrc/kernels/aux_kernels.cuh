@@ -46,6 +46,7 @@ __global__ void init_kernel(S* dist, unsigned long long n, unsigned long long so
   if (tid != 0) return;
   unsigned long long* ctl = p.ctl;
   ctl[C_STOP] = 0;
+  ctl[C_GEN] = 0;
   ctl[C_ERR] = 0;
   ctl[C_EPOCH] = 0;
   ctl[C_DIST_OVF] = 0;

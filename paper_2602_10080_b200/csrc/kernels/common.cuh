@@ -40,6 +40,7 @@ enum {
 enum : int {
   C_DONE = 0,             // global_done (l2.py:33-70), in queue units
   C_STOP = 16,            // work flag cleared by the manager (engine.py:152-169)
+  C_GEN = 17,             // work generation (same 16-byte pair as C_STOP: one idle poll)
   C_ERR = 32,             // ERR_* code
   C_EPOCH = 48,           // bucket floor index (l2.py:181-301)
   C_HUB_WP = 64,          // hub descriptor tickets issued
@@ -184,6 +185,14 @@ __device__ __forceinline__ Elem<unsigned long long> ld_cg_elem(const Elem<unsign
 __device__ __forceinline__ uint32_t ldcg_dist(const uint32_t* p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned long long ldcg_dist(const unsigned long long* p) { return __ldcg(p); }
 
+__device__ __forceinline__ void red_add(unsigned long long* a, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+// 16-byte relaxed load of two adjacent control words
+__device__ __forceinline__ void ld_relaxed_v2(const unsigned long long* p, unsigned long long& a,
+                                              unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
 // atomic min without a return value (RED.MIN at L2)
 __device__ __forceinline__ void red_min(uint32_t* a, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
@@ -279,7 +288,10 @@ struct KParams {
   int share;                    // eager spill to L2 when groups are idle (B200 extension)
   int fifo_park;                // FIFO readers take unconditional tickets
   int bscratch;                 // bucket writes use the per-warp histogram scratch (bmax <= 256)
+  int bwin;                     // bucket window: winners >= bwin buckets above the floor skip L0/L1 (0 = off)
   int batch_cap, out_cap, spill_cap;  // elements
+  int far_cap;                  // far staging elements (bucket window), 0 when unused
+  long long ring_margin;        // bucket rings: pending blocks kept free for racing writers
 };
 
 }  // namespace mlmq

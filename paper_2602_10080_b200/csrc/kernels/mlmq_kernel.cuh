@@ -34,10 +34,12 @@ struct Worker {
   E* spill;
   E* l1a;
   E* l1b;
+  E* fars;
   unsigned long long* met;
   unsigned long long* btick;  // bucket write scratch (smem): ticket base per bucket
   uint32_t* bhist;            // elements per bucket
   uint32_t* bcur;             // scatter cursor per bucket
+  uint32_t* bremap;           // bucket -> ring actually written (occupancy-aware)
   int lane, gid, L;
 
   // L0: per-lane register FIFO (shift register, pop at index 0)
@@ -70,11 +72,13 @@ struct Worker {
     l1a = spill + p.spill_cap;
     l1b = l1a + p.l1cap;
     const int l1n = (p.l1type == L1K_NEAR_FAR ? 2 : 1) * p.l1cap;
-    met = reinterpret_cast<unsigned long long*>(l1a + l1n);
+    fars = l1a + l1n;  // far staging (bucket window), p.far_cap elements
+    met = reinterpret_cast<unsigned long long*>(fars + p.far_cap);
     met[lane] = 0;  // metric + profile slots (kMetSlots == 32)
     btick = met + kMetSlots;
     bhist = reinterpret_cast<uint32_t*>(btick + (p.bscratch ? p.bmax : 0));
     bcur = bhist + (p.bscratch ? p.bmax : 0);
+    bremap = bcur + (p.bscratch ? p.bmax : 0);
     l0n = 0;
     wc = rc = l0size = 0;
     h1 = n1 = h2 = n2 = 0;
@@ -155,6 +159,12 @@ struct Worker {
     unsigned long long v = 0;
     if (lane == 0) v = ld_relaxed(a);
     return __shfl_sync(FULL, v, 0);
+  }
+  // Work generation (B200 extension): bumped after every publication of new shared work
+  // (ring block, hub descriptor, heap node, floor advance).  An idle group polls this
+  // one word (with the stop flag beside it) instead of re-walking the whole cascade.
+  __device__ __forceinline__ void bump_gen() const {
+    if (lane == 0) red_add(p.ctl + C_GEN, 1ull);
   }
   __device__ __forceinline__ unsigned long long* wp(int r) const { return p.ptrs + (size_t)r * 32; }
   __device__ __forceinline__ unsigned long long* rp(int r) const { return p.ptrs + (size_t)r * 32 + 16; }
@@ -315,6 +325,7 @@ struct Worker {
       st_release(p.seq + i, tk + 1);
     }
     __syncwarp();
+    bump_gen();
   }
 
   // Writer (l2.py:96-114): one fetch-add claims ceil(n/bs) tickets; all slot waits,
@@ -371,6 +382,7 @@ struct Worker {
     for (int k = lane; k < c; k += 32) dst[k] = ld_cg_elem(d + k);
     __syncwarp();
     if (lane == 0) st_release(p.seq + i, r + p.bn_mask + 1);
+    local_done += 1;  // every consumed ticket is one termination unit (l2.py:56-62)
     pcnt(P_NL2R, 1);
     return c;
   }
@@ -381,31 +393,57 @@ struct Worker {
     LOC();
     unsigned long long r = 0;
     int got = 0;
+    bool ok = true;
     if (lane == 0) {
       unsigned long long* rpp = rp(rid);
       unsigned long long* wpp = wp(rid);
       r = ld_relaxed(rpp);
       unsigned long long w = ld_relaxed(wpp);
-      while (r < w) {
-        LOC();
-        unsigned long long old = atomicCAS(rpp, r, r + 1);
-        if (old == r) { got = 1; break; }
-        if (kDebug && p.prof) met[kProfBase + P_CASFAIL] += 1;
-        r = old;
-        if (r >= w) w = ld_relaxed(wpp);
+      if (r < w) {
+        // One fetch-add claims a ticket (no CAS retry storm).  A racing reader can
+        // over-claim past the write pointer; it then either waits for the writer that
+        // already owns its ticket, or -- when the write pointer stands exactly at its
+        // ticket -- takes the ticket as a writer and publishes an EMPTY block, which it
+        // consumes itself (reserve and done both count it), so no claim is ever left
+        // dangling (the audit's "no pending tickets", engine.py:241-242).
+        r = atomicAdd(rpp, 1ull);
+        got = 1;
+        bool empty = false;
+        unsigned long long t0 = 0;
+        int spins = 0;
+        while ((w = ld_relaxed(wpp)) <= r) {
+          if (w == r && atomicCAS(wpp, r, r + 1) == r) { empty = true; break; }
+          if (++spins % 64 == 0) {
+            if (stopped()) { ok = false; break; }
+            const unsigned long long now = globaltimer_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > p.spin_timeout_ns) {
+              raise_error(ERR_OVERFLOW, (unsigned long long)rid, r & p.bn_mask, w, r);
+              ok = false;
+              break;
+            }
+          }
+          __nanosleep(32);
+        }
+        const unsigned long long slot = r & p.bn_mask;
+        if (ok && empty) {
+          ok = lane_spin(seq_ptr(rid, slot), r, rid, slot);  // slot free for ticket r
+          if (ok) {
+            p.cnt[(size_t)rid * (p.bn_mask + 1) + slot] = 0u;
+            st_release(seq_ptr(rid, slot), r + 1);
+          }
+        }
+        if (ok) {
+          wstate(W_RING_READ, r + 1);
+          ok = lane_spin(seq_ptr(rid, slot), r + 1, rid, slot);
+          wstate(W_NONE, 0);
+        }
       }
     }
     got = __shfl_sync(FULL, got, 0);
     if (!got) return 0;
     r = __shfl_sync(FULL, r, 0);
     count(M_L2A, 1);
-    const unsigned long long slot = r & p.bn_mask;
-    bool ok = true;
-    if (lane == 0) {
-      wstate(W_RING_READ, r + 1);
-      ok = lane_spin(seq_ptr(rid, slot), r + 1, rid, slot);
-      wstate(W_NONE, 0);
-    }
     if (!__shfl_sync(FULL, (int)ok, 0)) return 0;
     __syncwarp();
     return take_block(rid, r, dst);
@@ -439,13 +477,16 @@ struct Worker {
     const int x = emod + rel;
     return x >= p.bmax ? x - p.bmax : x;
   }
+  // l2.py:209-222 clamps far elements to bmax-1; with managed epochs that ring is the one
+  // just behind the floor (read first), so far elements clamp one ring earlier
+  __device__ __forceinline__ int rel_clamp() const { return p.bwin > 0 ? p.bmax - 2 : p.bmax - 1; }
   __device__ __forceinline__ int bucket_rel(S d, unsigned long long e) const {
     if (K == DK_F32) {
       const double base = (double)e * p.delta_f;
       const double dv = (double)__uint_as_float((uint32_t)d);
       if (dv < base) return 0;
       const double q = floor((dv - base) / p.delta_f);
-      return q >= (double)(p.bmax - 1) ? p.bmax - 1 : (int)q;
+      return q >= (double)rel_clamp() ? rel_clamp() : (int)q;
     } else {
       const unsigned long long base = e * p.delta_i;
       const unsigned long long dd = (unsigned long long)d;
@@ -456,7 +497,7 @@ struct Worker {
         q = (unsigned)diff / (unsigned)p.delta_i;  // 32-bit divide on the common path
       else
         q = diff / p.delta_i;
-      return q >= (unsigned long long)(p.bmax - 1) ? p.bmax - 1 : (int)q;
+      return q >= (unsigned long long)rel_clamp() ? rel_clamp() : (int)q;
     }
   }
 
@@ -498,12 +539,34 @@ struct Worker {
       return;
     }
     const int bs = p.bs;
-    for (int b = lane; b < p.bmax; b += 32) { bhist[b] = 0; bcur[b] = 0; }
+    // Occupancy-aware placement: a bucket ring that is nearly full (pending blocks within
+    // `ring_margin` of capacity) passes its elements on to the next ring.  Any ring is a
+    // correct home (the reader rebins or processes them), so a burst of far work can no
+    // longer wedge a writer on a full ring while the floor waits for near work.
+    for (int b = lane; b < p.bmax; b += 32) {
+      const unsigned long long occ = ld_relaxed(wp(b)) - ld_relaxed(rp(b));
+      bcur[b] = (long long)occ > (long long)(p.bn_mask + 1) - p.ring_margin ? 1u : 0u;
+      bhist[b] = 0;
+    }
+    __syncwarp();
+    for (int b = lane; b < p.bmax; b += 32) {
+      // move only farther from the floor and never past the clamp ring: an element is
+      // never placed where it would be rebinned straight back (no livelock)
+      int t = b;
+      int rel = b >= emod ? b - emod : b + p.bmax - emod;
+      while (bcur[t] && rel > 0 && rel < rel_clamp()) {
+        t = t + 1 == p.bmax ? 0 : t + 1;
+        ++rel;
+      }
+      bremap[b] = bcur[t] ? b : t;  // no room anywhere farther: keep the home ring (bounded wait)
+    }
+    __syncwarp();
+    for (int b = lane; b < p.bmax; b += 32) bcur[b] = 0;
     __syncwarp();
     for (int i = lane; i < n; i += 32) {
       LOC();
       const E x = base[(unsigned)(start + i) % (unsigned)cap];
-      atomicAdd(bhist + bring(emod, bucket_rel(x.d, e)), 1u);
+      atomicAdd(bhist + bremap[bring(emod, bucket_rel(x.d, e))], 1u);
     }
     __syncwarp();
     int used = 0;
@@ -534,7 +597,7 @@ struct Worker {
     for (int i = lane; i < n; i += 32) {
       LOC();
       const E x = base[(unsigned)(start + i) % (unsigned)cap];
-      const int f = bring(emod, bucket_rel(x.d, e));
+      const int f = bremap[bring(emod, bucket_rel(x.d, e))];
       const int r = (int)atomicAdd(bcur + f, 1u);
       const int sg = r / bs;
       slot_data(f, (btick[f] + sg) & p.bn_mask)[r - sg * bs] = x;
@@ -554,6 +617,7 @@ struct Worker {
       }
     }
     __syncwarp();
+    bump_gen();
   }
 
   // l2.py:235-295: scan bnum buckets from the floor; rebin stale-slot elements; advance
@@ -564,9 +628,12 @@ struct Worker {
     const unsigned long long e0 = warp_ld(p.ctl + C_EPOCH);
     const int e0mod = (int)(e0 % (unsigned long long)p.bmax);
     bool head_empty = false;
-    for (int j = 0; j < p.bnum; ++j) {
+    // managed epochs (bwin > 0): the ring just behind the floor is read first -- it holds
+    // elements binned against a floor that has since advanced
+    const int j0 = (p.bwin > 0 && p.bmax > 1) ? -1 : 0;
+    for (int j = j0; j < p.bnum; ++j) {
       LOC();
-      const int f = bring(e0mod, j);
+      const int f = j < 0 ? bring(e0mod, p.bmax - 1) : bring(e0mod, j);
       for (;;) {
         LOC();
         const int c = ring_read(f, dst);
@@ -574,7 +641,6 @@ struct Worker {
           if (j == 0) head_empty = true;
           break;
         }
-        local_done += 1;
         const unsigned long long en = warp_ld(p.ctl + C_EPOCH);
         const int enmod = (int)(en % (unsigned long long)p.bmax);
         const int rel_slot = f >= enmod ? f - enmod : f + p.bmax - enmod;
@@ -602,12 +668,15 @@ struct Worker {
         if (stopped_warp()) return 0;
       }
     }
-    if (head_empty) {
+    if (head_empty && p.bwin == 0) {  // managed epochs: only the manager advances the floor
       bool ne = false;
       for (int k = lane; k < p.bmax; k += 32)
         if (k != e0mod) ne |= ld_relaxed(wp(k)) > ld_relaxed(rp(k));
       if (__any_sync(FULL, ne)) {
-        if (lane == 0 && atomicCAS(p.ctl + C_EPOCH, e0, e0 + 1) == e0) met[M_L2A] += 1;
+        if (lane == 0 && atomicCAS(p.ctl + C_EPOCH, e0, e0 + 1) == e0) {
+          met[M_L2A] += 1;
+          red_add(p.ctl + C_GEN, 1ull);
+        }
         __syncwarp();
       }
     }
@@ -765,6 +834,7 @@ struct Worker {
       }
       count(M_L2A, 1);
       heap_unlock(h);
+      bump_gen();
     }
   }
   // l2.py:362-389: pop runs off the root while root.min <= min(child mins).
@@ -859,7 +929,6 @@ struct Worker {
     int c;
     if (L2K == L2K_FIFO) {
       c = p.fifo_park ? fifo_read(dst) : ring_read(0, dst);
-      if (c > 0) local_done += 1;
     } else if (L2K == L2K_BUCKET) {
       c = bucket_read(dst);
     } else {
@@ -1193,7 +1262,40 @@ struct Worker {
     CHKU();
   }
 
+  // B200 extension for the bucket L2 (Delta-stepping order): winners whose bucket lies
+  // bwin or more buckets above the current floor bypass the group-private L0/L1 and go
+  // straight to their L2 bucket, so the private levels only ever hold near-floor work
+  // and thousands of groups cannot run far ahead of the floor (work inflation).
+  __device__ void far_split() {
+    const unsigned long long e = warp_ld(p.ctl + C_EPOCH);
+    const int emod = (int)(e % (unsigned long long)p.bmax);
+    int kept = 0, nfar = 0;
+    for (int o = 0; o < outn; o += 32) {
+      const bool has = o + lane < outn;
+      E x = E();
+      int rel = 0;
+      if (has) {
+        x = outs[o + lane];
+        rel = bucket_rel(x.d, e);
+      }
+      __syncwarp();
+      const bool far = has && rel >= p.bwin;
+      const bool near = has && !far;
+      const unsigned nm = __ballot_sync(FULL, near);
+      if (near) outs[kept + __popc(nm & lanemask_lt())] = x;
+      kept += __popc(nm);
+      const unsigned fm = __ballot_sync(FULL, far);
+      if (far) fars[nfar + __popc(fm & lanemask_lt())] = x;
+      nfar += __popc(fm);
+      __syncwarp();
+    }
+    outn = kept;
+    // one histogram-grouped write: one ticket and full blocks per target bucket
+    if (nfar > 0) write_back(fars, 0, nfar, LINEAR);
+  }
+
   __device__ void flush_out(bool all) {
+    if (L2K == L2K_BUCKET && p.bwin > 0 && outn > 0) far_split();
     LOC();
     int d = 0;
     while (outn - d >= L) {
@@ -1332,6 +1434,7 @@ struct Worker {
         atomicExch(p.hub_next + slot, t << kClaimBits);
         __threadfence();
         st_release(p.hub_seq + slot, t + 1);
+        red_add(p.ctl + C_GEN, 1ull);
       }
     }
     __syncwarp();
@@ -1570,10 +1673,24 @@ struct Worker {
     int backoff = 0;
     const unsigned long long tstart = pclk();
     int since_check = 0;
+    unsigned long long seen = ~0ull;
     for (;;) {
       LOC();
-      // a busy warp polls the stop word every 16 iterations; an idle one every time
-      if ((idle || ++since_check >= 16)) {
+      if (idle) {
+        // idle: one 16-byte load of (generation, stop); re-walk the cascade only when
+        // new work was published since this group's last full miss
+        unsigned long long gen = 0, st = 0;
+        if (lane == 0) ld_relaxed_v2(p.ctl + C_STOP, st, gen);
+        st = __shfl_sync(FULL, st, 0);
+        gen = __shfl_sync(FULL, gen, 0);
+        if (st) break;
+        if (gen == seen) {
+          __nanosleep(32u << min(backoff, 5));
+          ++backoff;
+          continue;
+        }
+        seen = gen;
+      } else if (++since_check >= 16) {  // a busy group polls stop every 16 iterations
         since_check = 0;
         if (stopped_warp()) break;
       }
@@ -1606,6 +1723,7 @@ struct Worker {
       }
       if (!idle) {
         idle = true;
+        seen = ~0ull;  // the first miss re-checks once against a generation read before it
         if (lane == 0) atomicAdd(p.ctl + C_IDLE, 1ull);
       }
       // full miss: flush local_done (l2.py:56-62)
@@ -1647,7 +1765,7 @@ struct Worker {
 
 // K2: manager warp (engine.py:152-169): reserve == done on three consecutive polls.
 static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
-  int k = 0;
+  int k = 0, kq = 0;
   if ((kDebug && p.wstate) && lane == 0) p.wstate[2 * (size_t)p.G + 4] = 1;
   for (;;) {
     if (p.host_abort && lane == 0 && ld_sys_u32(p.host_abort) != 0u) {
@@ -1670,6 +1788,40 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
     if (lane == 0) r += ld_relaxed(p.ctl + C_HUB_RES);
     r = warp_sum_u64(r);
     k = (d == r) ? k + 1 : 0;
+    if (p.bwin > 0 && p.bmax > 2 && d != r) {
+      // Managed bucket floor (Delta-stepping order, B200 extension): all units not done
+      // are unclaimed blocks of rings other than the head and the ring behind it
+      // <=> the near window is quiescent (counters monotone, done read first).  Then
+      // the floor jumps to the first non-empty far bucket.
+      unsigned long long e = 0;
+      if (lane == 0) e = ld_relaxed(p.ctl + C_EPOCH);
+      e = __shfl_sync(FULL, e, 0);
+      const int emod = (int)(e % (unsigned long long)p.bmax);
+      unsigned long long far = 0;
+      int first = p.bmax;
+      for (int i = lane; i < p.nrings; i += 32) {
+        const int rel = i >= emod ? i - emod : i + p.bmax - emod;
+        if (rel == 0 || rel == p.bmax - 1) continue;
+        const unsigned long long w = ld_relaxed(p.ptrs + (size_t)i * 32);
+        const unsigned long long rd = ld_relaxed(p.ptrs + (size_t)i * 32 + 16);
+        if (w > rd) {
+          far += w - rd;
+          first = min(first, rel);
+        }
+      }
+      far = warp_sum_u64(far);
+      first = __reduce_min_sync(FULL, first);
+      kq = (far > 0 && d == r - far) ? kq + 1 : 0;
+      if (kq >= 2 && first < p.bmax) {
+        if (lane == 0) {
+          st_release(p.ctl + C_EPOCH, e + (unsigned long long)first);
+          red_add(p.ctl + C_GEN, 1ull);
+        }
+        kq = 0;
+      }
+    } else {
+      kq = 0;
+    }
     if ((kDebug && p.wstate) && lane == 0) {
       p.wstate[2 * (size_t)p.G] += 1;
       p.wstate[2 * (size_t)p.G + 2] = d;

@@ -184,7 +184,7 @@ struct LaunchShape {
   const void* fn = nullptr;
   int dk = 0, l2k = 0, cm = 4;
   int smem_per_warp = 0, wpb = 0;
-  int batch_cap = 0, spill_cap = 0;
+  int batch_cap = 0, spill_cap = 0, far_cap = 0;
   int max_groups = 0;
   int bscratch = 0;
 };
@@ -200,8 +200,9 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
   s->spill_cap = L * c->l0_capacity + L;
   const int l1n = (c->l1_type == MLMQ_L1_NEAR_FAR ? 2 : 1) * c->l1_capacity;
   s->bscratch = (s->l2k == L2K_BUCKET && c->bmax <= 256) ? 1 : 0;
-  long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n) + kMetSlots * 8 +
-                    (s->bscratch ? 16LL * c->bmax : 0LL);
+  s->far_cap = (s->l2k == L2K_BUCKET && c->bucket_window > 0 && c->bmax >= 3) ? kOutCap : 0;
+  long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n + s->far_cap) + kMetSlots * 8 +
+                    (s->bscratch ? 20LL * c->bmax : 0LL);
   bytes = (bytes + 15) / 16 * 16;
   int max_smem_block = 0;
   CK(cudaDeviceGetAttribute(&max_smem_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
@@ -227,7 +228,8 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
   return MLMQ_OK;
 }
 
-int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& sh, unsigned long long hub_chunk) {
+int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& sh, unsigned long long hub_chunk,
+                     int groups) {
   Workspace need;
   need.es = sh.dk == DK_U64 ? 16 : 8;
   need.bs = c->block_size;
@@ -241,7 +243,11 @@ int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& s
   } else {
     need.nrings = sh.l2k == L2K_BUCKET ? c->bmax : 1;
     const unsigned long long slots = 8ull * n / (unsigned long long)c->block_size + 16384ull;
-    unsigned long long per = sh.l2k == L2K_BUCKET ? slots / 8 + 1024 : slots;
+    // bucket rings: a quarter of the FIFO ring each, and room for every group to race
+    // a few blocks into a ring past the occupancy check (ring_margin)
+    unsigned long long per = sh.l2k == L2K_BUCKET
+                                 ? std::max<unsigned long long>(slots / 4 + 1024, 16ull * (unsigned long long)groups + 1024ull)
+                                 : slots;
     need.bn = next_pow2(std::max<unsigned long long>((unsigned long long)c->block_num, per));
     need.nheaps = 0;
     need.hcap = 0;
@@ -411,7 +417,7 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     return MLMQ_EINVAL;
   }
   const unsigned long long hub_chunk = c->hub_chunk > 0 ? std::min<unsigned long long>((unsigned long long)c->hub_chunk, 1ull << 20) : 3072ull;
-  if ((st = ensure_workspace(g, c, sh, hub_chunk))) return st;
+  if ((st = ensure_workspace(g, c, sh, hub_chunk, G))) return st;
   if (g->metrics_cap < (unsigned long long)G) {
     cudaFree(g->d_metrics);
     g->d_metrics = nullptr;
@@ -500,9 +506,12 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.batch_cap = sh.batch_cap;
   p.out_cap = kOutCap;
   p.spill_cap = sh.spill_cap;
+  p.far_cap = sh.far_cap;
+  p.ring_margin = std::min<long long>((long long)w.bn / 2, 4LL * G + 64);
   p.share = c->share ? 1 : 0;
   p.fifo_park = (sh.l2k == L2K_FIFO && c->fifo_park) ? 1 : 0;
   p.bscratch = sh.bscratch;
+  p.bwin = (sh.l2k == L2K_BUCKET && c->bmax >= 3) ? std::max(0, c->bucket_window) : 0;
 
   *g->h_abort = 0;
   const int blocks = (G + 1 + sh.wpb - 1) / sh.wpb;

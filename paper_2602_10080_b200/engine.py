@@ -47,6 +47,7 @@ class EngineConfig:
     device: int = 0
     share: bool = True       # eager write-back to L2 while groups idle (B200 extension)
     fifo_park: bool = True   # FIFO readers park on unconditional tickets
+    bucket_window: int = 1   # bucket L2: winners >= this many buckets above the floor skip L0/L1
 
 
 class SsspResult:
@@ -179,6 +180,7 @@ def _native_config(cfg: MlmqConfig, eng: EngineConfig, unit_weights: bool,
     c.hub_chunk = int(eng.hub_chunk)
     c.share = 1 if eng.share else 0
     c.fifo_park = 1 if eng.fifo_park else 0
+    c.bucket_window = max(0, int(eng.bucket_window))
     return c
 
 
