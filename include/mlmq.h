@@ -160,6 +160,29 @@ int mlmq_last_dist(mlmq_graph* g, uint64_t* dist_out);
 int mlmq_reach(mlmq_graph* g, uint64_t* v_reach, uint64_t* e_reach);
 
 /*
+ * Sharded solve (the reference has none -- PAPER.md:797 names a multi-GPU
+ * "L3 queue" as future work).  1D vertex partition: shard `rank` of `nparts` (a power of
+ * two <= 64) owns global vertices v with v mod nparts == rank, stored at local id
+ * v / nparts.  row_offsets/w are the owned rows in local order; col holds GLOBAL ids.
+ * A solve is a sequence of supersteps driven by the host (one process per GPU,
+ * exchanging the send buffers with an all-to-all):
+ *   mlmq_shard_begin(g)                        dist = ghost = INF
+ *   mlmq_shard_step(g, cfg, inbox, n_in, ...)  apply the inbox (device pairs of (global v,
+ *       d) owned by this shard, e.g. (source, 0) on its owner for the first step), run K1 to
+ *       local quiescence, then write the remote improvements grouped by owner into the
+ *       caller's DEVICE buffer d_send (send_cap pairs) and their per-owner counts into
+ *       send_counts[nparts] (host).  The solve is done when no shard sends anything.
+ * Distances: mlmq_last_dist (local order), mlmq_reach (this shard's V/E_reach).
+ */
+int mlmq_shard_create(const uint64_t* row_offsets, const uint32_t* col, const void* w, int weight_kind,
+                      uint64_t n_local, uint64_t m_local, uint64_t n_global, uint32_t rank,
+                      uint32_t nparts, int device, mlmq_graph** out);
+int mlmq_shard_begin(mlmq_graph* g);
+int mlmq_shard_step(mlmq_graph* g, const mlmq_config_t* cfg, const uint32_t* d_inbox, uint64_t n_in,
+                    uint32_t* d_send, uint64_t send_cap, uint64_t* send_counts,
+                    mlmq_metrics_t* metrics_out);
+
+/*
  * K4: the 8 selector features (graph.py:428-460) as exact integer sums:
  * out[0]=n out[1]=m out[2]=sum deg out[3]=sum deg^2 (lo) out[4]=sum deg^2 (hi)
  * out[5]=max deg out[6]=sum w out[7]=sum w^2 (lo) out[8]=sum w^2 (hi) out[9]=max w.

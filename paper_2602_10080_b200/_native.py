@@ -73,7 +73,7 @@ EXPORTED_SYMBOLS = (
     "mlmq_graph_create", "mlmq_graph_destroy", "mlmq_graph_device_bytes", "mlmq_auto_groups",
     "mlmq_sssp", "mlmq_sssp_f32", "mlmq_sssp_device", "mlmq_last_dist", "mlmq_reach",
     "mlmq_feature_sums", "mlmq_gen_size", "mlmq_gen_graph", "mlmq_build_csr",
-    "mlmq_gen_f32_weights",
+    "mlmq_gen_f32_weights", "mlmq_shard_create", "mlmq_shard_begin", "mlmq_shard_step",
 )
 
 _lib = None
@@ -116,6 +116,9 @@ def lib():
             "mlmq_gen_graph": ([I32, P, P, U64, P, P, P], I32),
             "mlmq_build_csr": ([U64, U64, P, P, P, P, P, P, P], I32),
             "mlmq_gen_f32_weights": ([U64, U64, P], I32),
+            "mlmq_shard_create": ([P, P, P, I32, U64, U64, U64, ctypes.c_uint32, ctypes.c_uint32, I32, P], I32),
+            "mlmq_shard_begin": ([P], I32),
+            "mlmq_shard_step": ([P, P, P, U64, P, U64, P, P], I32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -234,6 +237,45 @@ class DeviceGraph:
         out = ctypes.c_uint64()
         check(self._lib.mlmq_graph_device_bytes(self.handle, ctypes.byref(out)))
         return int(out.value)
+
+
+class DeviceShard(DeviceGraph):
+    """One shard of a 1D-partitioned graph (include/mlmq.h mlmq_shard_*): owned rows in
+    local order, GLOBAL column ids."""
+
+    def __init__(self, row_offsets: np.ndarray, col: np.ndarray, weights: Optional[np.ndarray],
+                 weight_kind: int, n_global: int, rank: int, nparts: int, device: int = 0):
+        L = lib()
+        if device_count() < 1:
+            raise EngineError("no CUDA device is visible; the MLMQ engine has no CPU fallback")
+        self._lib = L
+        self.row_offsets = np.ascontiguousarray(row_offsets, dtype=np.uint64)
+        self.col = np.ascontiguousarray(col, dtype=np.uint32)
+        self.n = int(self.row_offsets.size - 1)
+        self.m = int(self.col.size)
+        self.weight_kind = weight_kind
+        self.n_global, self.rank, self.nparts = int(n_global), int(rank), int(nparts)
+        w = None
+        if weight_kind == W_U32:
+            w = np.ascontiguousarray(weights, dtype=np.uint32)
+        elif weight_kind == W_F32:
+            w = np.ascontiguousarray(weights, dtype=np.float32)
+        h = ctypes.c_void_p()
+        check(L.mlmq_shard_create(_ptr(self.row_offsets), _ptr(self.col), _ptr(w), weight_kind, self.n,
+                                  self.m, self.n_global, self.rank, self.nparts, device, ctypes.byref(h)))
+        self.handle = h
+
+    def begin(self) -> None:
+        check(self._lib.mlmq_shard_begin(self.handle))
+
+    def step(self, cfg: Config, inbox_ptr: int, n_in: int, send_ptr: int, send_cap: int):
+        """One superstep; inbox/send are DEVICE pointers to (v, d) u32 pairs.  Returns
+        (per-owner send counts, Metrics)."""
+        counts = np.zeros(self.nparts, dtype=np.uint64)
+        m = Metrics()
+        check(self._lib.mlmq_shard_step(self.handle, ctypes.byref(cfg), inbox_ptr or None, int(n_in),
+                                        send_ptr, int(send_cap), _ptr(counts), ctypes.byref(m)))
+        return counts, m
 
 
 def seed_key(seed: int) -> np.ndarray:

@@ -37,12 +37,15 @@ __global__ void reset_queues_kernel(unsigned long long* seq, unsigned long long 
 // K3 (DistanceTable.__init__ core.py:198-203 + mlmq_bootstrap compose.py:92-101):
 // dist = INF except dist[s] = 0; control words reset; done := current reserve total;
 // (s, 0) written straight through to the L2 queue.
+// step = 1: a superstep of a sharded solve -- distances persist, no bootstrap (the
+// seeds arrive through seed_* below).
 template <class S>
 __global__ void init_kernel(S* dist, unsigned long long n, unsigned long long source, S inf,
-                            KParams p, int l2k) {
+                            KParams p, int l2k, int step = 0) {
   const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long i = tid; i < n; i += stride) dist[i] = (i == source) ? (S)0 : inf;
+  if (!step)
+    for (unsigned long long i = tid; i < n; i += stride) dist[i] = (i == source) ? (S)0 : inf;
   if (tid != 0) return;
   unsigned long long* ctl = p.ctl;
   ctl[C_STOP] = 0;
@@ -59,6 +62,10 @@ __global__ void init_kernel(S* dist, unsigned long long n, unsigned long long so
   for (int r = 0; r < p.nrings; ++r) reserve += p.ptrs[(size_t)r * 32];
   for (int h = 0; h < p.pnum; ++h) reserve += p.hwc[(size_t)h * 16];
   ctl[C_DONE] = reserve;
+  if (step) {
+    __threadfence();
+    return;
+  }
   if (l2k == L2K_HEAP) {
     Elem<S> e;
     e.v = (uint32_t)source;
@@ -132,6 +139,107 @@ __global__ void audit_kernel(KParams p, unsigned long long* out, int fifo_fix) {
       __threadfence();
     }
     if (kDebug && p.wstate) p.wstate[2 * (size_t)p.G + 5] = 2;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Sharded solve: superstep plumbing around K1
+// ---------------------------------------------------------------------------------
+template <class S>
+__global__ void fill_kernel(S* a, unsigned long long n, S v) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n; i += stride) a[i] = v;
+}
+
+// Apply the inbox (global v, d) to this shard's distances; improved vertices become
+// seeds (local id, d).  scratch[0] = seed count.
+template <class S>
+__global__ void seed_apply_kernel(const uint2* inbox, unsigned long long n_in, S* dist, int shift,
+                                  unsigned long long n_local, uint2* seeds, unsigned long long* scratch,
+                                  unsigned long long* err) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n_in; i += stride) {
+    const uint2 m = inbox[i];
+    const unsigned long long lv = (unsigned long long)(m.x >> shift);
+    if (lv >= n_local) {
+      atomicCAS(err, 0ull, (unsigned long long)ERR_CORRUPT);
+      continue;
+    }
+    if ((S)m.y < atomicMin(dist + lv, (S)m.y)) {
+      const unsigned long long k = atomicAdd(scratch, 1ull);
+      seeds[k] = make_uint2((uint32_t)lv, m.y);
+    }
+  }
+}
+
+// Write the seeds into L2 ring 0 as full blocks (write_through, compose.py:79-86): the
+// write tickets are the reservation (the init kernel already set done = reserve).
+template <class S>
+__global__ void seed_ring_kernel(const uint2* seeds, const unsigned long long* scratch, KParams p) {
+  __shared__ unsigned long long t0;
+  const unsigned long long ns = scratch[0];
+  const unsigned long long nblk = (ns + p.bs - 1) / p.bs;
+  if (threadIdx.x == 0) t0 = p.ptrs[0];
+  __syncthreads();
+  for (unsigned long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const unsigned long long tk = t0 + b, slot = tk & p.bn_mask;
+    const unsigned long long lo = b * p.bs, c = min((unsigned long long)p.bs, ns - lo);
+    Elem<S>* dst = reinterpret_cast<Elem<S>*>(p.data) + slot * p.bs;
+    for (unsigned long long i = threadIdx.x; i < c; i += blockDim.x) {
+      Elem<S> e;
+      e.v = seeds[lo + i].x;
+      e.d = (S)seeds[lo + i].y;
+      dst[i] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (p.seq[slot] != tk) atomicCAS(p.ctl + C_ERR, 0ull, (unsigned long long)ERR_CORRUPT);
+      p.cnt[slot] = (uint32_t)c;
+      __threadfence();
+      p.seq[slot] = tk + 1;
+    }
+    __syncthreads();
+  }
+}
+__global__ void seed_commit_kernel(const unsigned long long* scratch, KParams p) {
+  const unsigned long long nblk = (scratch[0] + p.bs - 1) / p.bs;
+  p.ptrs[0] += nblk;
+  __threadfence();
+}
+
+// Group the outbox by owner shard (counting sort): send[] = concatenation per rank,
+// counts[r] = pairs for rank r.  scratch layout: [0] outbox fill, [8..8+P) counts,
+// [72..72+P) cursors.
+__global__ void obox_hist_kernel(const uint2* obox, const unsigned long long* scratch_n, unsigned long long cap,
+                                 unsigned long long* counts, uint32_t pmask) {
+  __shared__ unsigned int h[64];
+  if (threadIdx.x < 64) h[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned long long n = min(*scratch_n, cap);  // an overflowing step is an error anyway
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n; i += stride) atomicAdd(h + (obox[i].x & pmask), 1u);
+  __syncthreads();
+  if (threadIdx.x <= pmask && h[threadIdx.x]) atomicAdd(counts + threadIdx.x, (unsigned long long)h[threadIdx.x]);
+}
+__global__ void obox_scan_kernel(const unsigned long long* counts, unsigned long long* cursors, int P) {
+  unsigned long long s = 0;
+  for (int r = 0; r < P; ++r) {
+    cursors[r] = s;
+    s += counts[r];
+  }
+}
+__global__ void obox_scatter_kernel(const uint2* obox, const unsigned long long* scratch_n,
+                                    unsigned long long cap, unsigned long long* cursors, uint2* send,
+                                    uint32_t pmask) {
+  const unsigned long long n = min(*scratch_n, cap);
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n; i += stride) {
+    const uint2 m = obox[i];
+    send[atomicAdd(cursors + (m.x & pmask), 1ull)] = m;
   }
 }
 

@@ -33,7 +33,8 @@ enum {
   ERR_ABORT = 2,         // host watchdog abort (engine.py:267-272)
   ERR_HEAP_OVERFLOW = 3, // batch-heap node pool exhausted
   ERR_HUB_OVERFLOW = 4,  // hub work ring slot stayed busy
-  ERR_CORRUPT = 5        // a queue element named a vertex >= n (internal error)
+  ERR_CORRUPT = 5,       // a queue element named a vertex >= n (internal error)
+  ERR_OBOX = 6           // sharded solve: remote-update outbox full
 };
 
 // Control block: u64 words, every hot word on its own 128-byte line.
@@ -292,6 +293,15 @@ struct KParams {
   int batch_cap, out_cap, spill_cap;  // elements
   int far_cap;                  // far staging elements (bucket window), 0 when unused
   long long ring_margin;        // bucket rings: pending blocks kept free for racing writers
+
+  // 1D-partitioned shard; nparts == 1 for an unpartitioned graph
+  int nparts;                   // P (power of two)
+  int part_shift;               // log2 P
+  uint32_t rank;                // this shard
+  void* ghost;                  // S[n_global]: ghost distances of remote vertices
+  uint2* obox;                  // outbox of remote improvements (global v, d)
+  unsigned long long* obox_n;   // outbox fill
+  unsigned long long obox_cap;
 };
 
 }  // namespace mlmq

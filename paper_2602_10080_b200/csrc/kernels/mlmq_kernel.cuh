@@ -1338,6 +1338,7 @@ struct Worker {
         if (nd[j] == (S)Tr::INF) act[j] = false;
       }
     }
+    if (p.nparts > 1) relax_remote(act, v, nd);  // 1D-partitioned shard
 #pragma unroll
     for (int j = 0; j < U; ++j)
       if (act[j]) act[j] = nd[j] < ldcg_dist(dist + v[j]);
@@ -1366,6 +1367,52 @@ struct Worker {
     n_upd += (unsigned)upd;  // warp total, lane-replicated
     __syncwarp();
     if (outn >= L) flush_out(false);
+  }
+
+  // Sharded solve: this group's shard owns global vertices v with
+  // v mod P == rank (local id v / P).  Local targets are remapped to local ids and relax
+  // as usual; a remote target is pruned against the shard's ghost copy of remote
+  // distances (a ghost is never below the true distance, so nd >= ghost[v] is safely
+  // dropped), and an improving remote relaxation is appended to the outbox as
+  // (global v, nd) -- one fetch-add per warp and step -- for the owner to apply after
+  // the superstep's exchange.
+  __device__ void relax_remote(bool (&act)[U], uint32_t (&v)[U], const S (&nd)[U]) {
+    const uint32_t pmask = (uint32_t)p.nparts - 1u;
+    S* ghost = reinterpret_cast<S*>(p.ghost);
+    bool em[U];
+    int tot = 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      em[j] = false;
+      if (act[j]) {
+        if ((v[j] & pmask) == p.rank) {
+          v[j] >>= p.part_shift;
+        } else {
+          act[j] = false;
+          em[j] = nd[j] < ldcg_dist(ghost + v[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (em[j]) em[j] = nd[j] < atomicMin(ghost + v[j], nd[j]);
+#pragma unroll
+    for (int j = 0; j < U; ++j) tot += __popc(__ballot_sync(FULL, em[j]));
+    if (tot == 0) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(p.obox_n, (unsigned long long)tot);
+    base = __shfl_sync(FULL, base, 0);
+    if (base + (unsigned long long)tot > p.obox_cap) {
+      if (lane == 0) raise_error(ERR_OBOX, base + tot, p.obox_cap, 0, 0);
+      return;
+    }
+    int off = 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const unsigned m = __ballot_sync(FULL, em[j]);
+      if (em[j]) p.obox[base + off + __popc(m & lanemask_lt())] = make_uint2(v[j], (uint32_t)nd[j]);
+      off += __popc(m);
+    }
   }
 
   // the whole warp strides one edge list (engine.py:212-220 "big" tier, hub chunks)

@@ -142,6 +142,25 @@ struct mlmq_graph {
   Workspace ws;
   int last_dk = -1;
   std::mutex mu;
+  // sharded solve: 1D partition, v -> shard v mod P, local id v / P
+  uint32_t nparts = 1, rank = 0;
+  int shift = 0;
+  unsigned long long n_global = 0;
+  void* d_ghost = nullptr;                // S[n_global]
+  uint2* d_obox = nullptr;                // remote-update outbox
+  unsigned long long obox_cap = 0;
+  uint2* d_seeds = nullptr;               // improved inbox entries (<= inbox size)
+  unsigned long long seeds_cap = 0;
+  unsigned long long* d_sscratch = nullptr;  // [0] outbox fill [1] seed count [8..] counts [72..] cursors
+};
+
+// Inputs/outputs of one superstep of a sharded solve.
+struct ShardIo {
+  const uint2* inbox = nullptr;
+  unsigned long long n_in = 0;
+  uint2* send = nullptr;
+  unsigned long long send_cap = 0;
+  uint64_t* send_counts = nullptr;  // host [nparts]
 };
 
 namespace {
@@ -407,7 +426,7 @@ void debug_dump(mlmq_graph* g, int G, const char* tag) {
 // One attempt at a given distance kind.  Returns MLMQ_OK, an error, or 100 when the
 // optimistic u32 distances overflowed (caller re-runs in u64).
 int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, int dk,
-             mlmq_metrics_t* mo, uint64_t* gm, uint64_t gm_cap) {
+             mlmq_metrics_t* mo, uint64_t* gm, uint64_t gm_cap, const ShardIo* io = nullptr) {
   LaunchShape sh;
   int st = launch_shape(g, c, dk, &sh);
   if (st) return st;
@@ -512,22 +531,49 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.fifo_park = (sh.l2k == L2K_FIFO && c->fifo_park) ? 1 : 0;
   p.bscratch = sh.bscratch;
   p.bwin = (sh.l2k == L2K_BUCKET && c->bmax >= 3) ? std::max(0, c->bucket_window) : 0;
+  p.nparts = (int)g->nparts;
+  p.part_shift = g->shift;
+  p.rank = g->rank;
+  p.ghost = g->d_ghost;
+  p.obox = g->d_obox;
+  p.obox_n = g->d_sscratch;
+  p.obox_cap = g->obox_cap;
 
   *g->h_abort = 0;
   const int blocks = (G + 1 + sh.wpb - 1) / sh.wpb;
   const int init_blocks = (int)std::min<unsigned long long>(4ull * g->sm_count, (g->n + 255) / 256 + 1);
   CK(cudaEventRecord(g->ev0, g->stream));
+  const int step = io ? 1 : 0;
   if (dk == DK_U64)
-    init_kernel<unsigned long long><<<init_blocks, 256, 0, g->stream>>>((unsigned long long*)g->d_dist, g->n, source, ~0ull, p, sh.l2k);
+    init_kernel<unsigned long long><<<init_blocks, 256, 0, g->stream>>>((unsigned long long*)g->d_dist, g->n, source, ~0ull, p, sh.l2k, step);
   else
     init_kernel<uint32_t><<<init_blocks, 256, 0, g->stream>>>((uint32_t*)g->d_dist, g->n, source,
-                                                              dk == DK_F32 ? 0x7f800000u : 0xFFFFFFFFu, p, sh.l2k);
+                                                              dk == DK_F32 ? 0x7f800000u : 0xFFFFFFFFu, p, sh.l2k, step);
   CK(cudaGetLastError());
+  if (io) {  // superstep: apply the inbox, seed ring 0 with the improved vertices
+    CK(cudaMemsetAsync(g->d_sscratch, 0, 256 * 8, g->stream));
+    if (io->n_in) {
+      const int sb = (int)std::min<unsigned long long>(8ull * g->sm_count, (io->n_in + 255) / 256 + 1);
+      seed_apply_kernel<uint32_t><<<sb, 256, 0, g->stream>>>(io->inbox, io->n_in, (uint32_t*)g->d_dist, g->shift, g->n,
+                                                            g->d_seeds, g->d_sscratch + 1, g->d_ctl + C_ERR);
+      seed_ring_kernel<uint32_t><<<2 * g->sm_count, 256, 0, g->stream>>>(g->d_seeds, g->d_sscratch + 1, p);
+      seed_commit_kernel<<<1, 1, 0, g->stream>>>(g->d_sscratch + 1, p);
+      CK(cudaGetLastError());
+    }
+  }
   void* args[] = {(void*)&p};
   CK(cudaLaunchCooperativeKernel(sh.fn, dim3(blocks), dim3(sh.wpb * 32), args,
                                  (size_t)sh.wpb * sh.smem_per_warp, g->stream));
   audit_kernel<<<1, 256, 0, g->stream>>>(p, g->d_audit, p.fifo_park);
   CK(cudaGetLastError());
+  if (io) {  // group the outbox by owner shard into the caller's send buffer
+    const uint32_t pmask = g->nparts - 1;
+    const int ob = 2 * g->sm_count;
+    obox_hist_kernel<<<ob, 256, 0, g->stream>>>(g->d_obox, g->d_sscratch, g->obox_cap, g->d_sscratch + 8, pmask);
+    obox_scan_kernel<<<1, 1, 0, g->stream>>>(g->d_sscratch + 8, g->d_sscratch + 72, (int)g->nparts);
+    obox_scatter_kernel<<<ob, 256, 0, g->stream>>>(g->d_obox, g->d_sscratch, g->obox_cap, g->d_sscratch + 72, io->send, pmask);
+    CK(cudaGetLastError());
+  }
   CK(cudaEventRecord(g->ev1, g->stream));
 
   // host watchdog (engine.py:267-279)
@@ -591,6 +637,12 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     set_last_error("hub work ring slot %llu stayed busy for %gs (capacity %llu)", au[9], spin, au[11]);
     return MLMQ_EOVERFLOW;
   }
+  if (err == ERR_OBOX) {
+    w.dirty = true;
+    set_last_error("sharded solve: remote-update outbox full (%llu of %llu pairs); raise the send capacity",
+                   au[8], au[9]);
+    return MLMQ_EOVERFLOW;
+  }
   if (err == ERR_CORRUPT) {
     w.dirty = true;
     set_last_error("internal error: corrupt queue state code=%llu value=%llu (n=%llu) group=%llu extra=%llu",
@@ -649,6 +701,10 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     const size_t cnt = std::min<size_t>((size_t)gm_cap, (size_t)G) * M_COUNT;
     std::memcpy(gm, hm.data(), cnt * 8);
   }
+  if (io && io->send_counts) {
+    CK(cudaMemcpy(io->send_counts, g->d_sscratch + 8, (size_t)g->nparts * 8, cudaMemcpyDeviceToHost));
+    io->send_counts[g->rank] = 0;  // never produced (own vertices relax locally)
+  }
   g->last_dk = dk;
   return MLMQ_OK;
 }
@@ -674,6 +730,10 @@ int solve(mlmq_graph* g, uint64_t source, const mlmq_config_t* c, void* dist_out
   const double t0 = now_s();
   std::lock_guard<std::mutex> lk(g->mu);
   CK(cudaSetDevice(g->device));
+  if (g->nparts > 1) {
+    set_last_error("this graph is a shard of a partitioned graph: use mlmq_shard_step");
+    return MLMQ_EINVAL;
+  }
   if (source >= g->n) {
     set_last_error("source %llu out of range for %llu vertices", (unsigned long long)source, g->n);
     return MLMQ_EINVAL;
@@ -838,6 +898,10 @@ void mlmq_graph_destroy(mlmq_graph* g) {
   cudaFree(g->d_scratch);
   cudaFree(g->d_prof);
   cudaFree(g->d_wstate);
+  cudaFree(g->d_ghost);
+  cudaFree(g->d_obox);
+  cudaFree(g->d_seeds);
+  cudaFree(g->d_sscratch);
   if (g->h_abort) cudaFreeHost(g->h_abort);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
@@ -911,6 +975,98 @@ int mlmq_reach(mlmq_graph* g, uint64_t* v_reach, uint64_t* e_reach) {
   CK(cudaStreamSynchronize(g->stream));
   *v_reach = h[0];
   *e_reach = h[1];
+  return MLMQ_OK;
+}
+
+int mlmq_shard_create(const uint64_t* row_offsets, const uint32_t* col, const void* w, int weight_kind,
+                      uint64_t n_local, uint64_t m_local, uint64_t n_global, uint32_t rank, uint32_t nparts,
+                      int device, mlmq_graph** out) {
+  if (!out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  if (nparts < 1 || nparts > 64 || (nparts & (nparts - 1)) || rank >= nparts) {
+    set_last_error("nparts must be a power of two in [1, 64] and rank < nparts (got %u, %u)", nparts, rank);
+    return MLMQ_EINVAL;
+  }
+  if (n_global == 0 || n_global > 0xFFFFFFFFull || n_local != (n_global - rank + nparts - 1) / nparts) {
+    set_last_error("shard %u of %u must own ceil((n - rank) / nparts) = %llu vertices (got %llu)", rank, nparts,
+                   (unsigned long long)((n_global - rank + nparts - 1) / nparts), (unsigned long long)n_local);
+    return MLMQ_EINVAL;
+  }
+  int st = mlmq_graph_create(row_offsets, col, w, weight_kind, n_local, m_local, device, out);
+  if (st) return st;
+  mlmq_graph* g = *out;
+  g->nparts = nparts;
+  g->rank = rank;
+  while ((1u << g->shift) < nparts) ++g->shift;
+  g->n_global = n_global;
+  cudaError_t e = cudaMalloc(&g->d_ghost, n_global * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&g->d_sscratch, 256 * 8);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    mlmq_graph_destroy(g);
+    *out = nullptr;
+    set_last_error("shard allocation failed: %s", cudaGetErrorString(e));
+    return MLMQ_ENOMEM;
+  }
+  return MLMQ_OK;
+}
+
+int mlmq_shard_begin(mlmq_graph* g) {
+  if (!g || g->nparts < 1 || !g->d_ghost) { set_last_error("not a shard"); return MLMQ_EINVAL; }
+  std::lock_guard<std::mutex> lk(g->mu);
+  CK(cudaSetDevice(g->device));
+  const uint32_t inf = g->wkind == MLMQ_W_F32 ? 0x7f800000u : 0xFFFFFFFFu;
+  const int b = 4 * g->sm_count;
+  fill_kernel<uint32_t><<<b, 256, 0, g->stream>>>((uint32_t*)g->d_dist, g->n, inf);
+  fill_kernel<uint32_t><<<b, 256, 0, g->stream>>>((uint32_t*)g->d_ghost, g->n_global, inf);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(g->stream));
+  g->last_dk = g->wkind == MLMQ_W_F32 ? DK_F32 : DK_U32;
+  return MLMQ_OK;
+}
+
+int mlmq_shard_step(mlmq_graph* g, const mlmq_config_t* c, const uint32_t* d_inbox, uint64_t n_in,
+                    uint32_t* d_send, uint64_t send_cap, uint64_t* send_counts, mlmq_metrics_t* metrics_out) {
+  if (!g || !c || !send_counts || (n_in && !d_inbox) || !d_send) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  if (!g->d_ghost) { set_last_error("not a shard: create it with mlmq_shard_create"); return MLMQ_EINVAL; }
+  if (c->l2_type != MLMQ_L2_FIFO) { set_last_error("sharded solves run the FIFO L2 (got l2_type code %d)", c->l2_type); return MLMQ_EINVAL; }
+  if (c->dist_mode == MLMQ_DIST_U64) { set_last_error("sharded solves keep u32 / f32 distances"); return MLMQ_EINVAL; }
+  const double t0 = now_s();
+  std::lock_guard<std::mutex> lk(g->mu);
+  CK(cudaSetDevice(g->device));
+  int st = validate(c);
+  if (st) return st;
+  if (g->obox_cap < send_cap) {
+    cudaFree(g->d_obox);
+    g->d_obox = nullptr;
+    g->obox_cap = 0;
+    CK(cudaMalloc(&g->d_obox, std::max<size_t>(8, send_cap * 8)));
+    g->obox_cap = send_cap;
+  }
+  if (g->seeds_cap < n_in) {  // an inbox may improve one vertex several times
+    cudaFree(g->d_seeds);
+    g->d_seeds = nullptr;
+    g->seeds_cap = 0;
+    CK(cudaMalloc(&g->d_seeds, std::max<size_t>(8, n_in * 8)));
+    g->seeds_cap = n_in;
+  }
+  ShardIo io;
+  io.inbox = reinterpret_cast<const uint2*>(d_inbox);
+  io.n_in = n_in;
+  io.send = reinterpret_cast<uint2*>(d_send);
+  io.send_cap = send_cap;
+  io.send_counts = send_counts;
+  const int dk = g->wkind == MLMQ_W_F32 ? DK_F32 : DK_U32;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    st = run_once(g, 0, c, dk, metrics_out, nullptr, 0, &io);
+    if (st == 101) continue;
+    break;
+  }
+  if (st == 100) {
+    set_last_error("sharded solve: a distance overflowed u32 (use an unpartitioned u64 solve)");
+    return MLMQ_EOVERFLOW;
+  }
+  if (st) return st;
+  if (metrics_out) metrics_out->wall_time_us = (uint64_t)((now_s() - t0) * 1e6);
   return MLMQ_OK;
 }
 
