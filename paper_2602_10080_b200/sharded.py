@@ -148,6 +148,34 @@ class ShardedResult:
     local_dist: np.ndarray
     steps: int
     sent: int
+    kernel_ms: float = 0.0    # superstep kernels (library CUDA events), this rank / all shards
+    exchange_ms: float = 0.0  # all-to-all + termination all-reduce (CUDA events on torch's stream)
+
+
+def _backend_ms(backend) -> float:
+    f = getattr(backend, "kernel_ms", None)
+    return float(f()) if f else 0.0
+
+
+class _Clock:
+    """Accumulates device time of the exchange phases on torch's current stream."""
+
+    def __init__(self, device):
+        import torch
+        self.on = device.type == "cuda"
+        self.ms = 0.0
+        if self.on:
+            self.a, self.b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def start(self):
+        if self.on:
+            self.a.record()
+
+    def stop(self):
+        if self.on:
+            self.b.record()
+            self.b.synchronize()
+            self.ms += self.a.elapsed_time(self.b)
 
 
 def solve_distributed(backend, source: int, group=None, max_steps: int = 1 << 20) -> ShardedResult:
@@ -161,23 +189,27 @@ def solve_distributed(backend, source: int, group=None, max_steps: int = 1 << 20
     backend.begin()
     inbox = _source_inbox(backend, source, P, r)
     steps = sent = 0
+    clk = _Clock(dev)
     while steps < max_steps:
         send, counts = backend.step(inbox)
         steps += 1
+        clk.start()
         c = torch.tensor(counts, dtype=torch.int64, device=dev)
         rc = torch.empty_like(c)
         dist.all_to_all_single(rc, c, group=group)
         total = c.sum().reshape(1).clone()
         dist.all_reduce(total, group=group)
         if int(total.item()) == 0:
+            clk.stop()
             break
         rcounts = [int(x) for x in rc.tolist()]
         recv = torch.empty(2 * sum(rcounts), dtype=torch.int32, device=dev)
         dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=[2 * x for x in rcounts],
                                input_split_sizes=[2 * x for x in counts], group=group)
+        clk.stop()
         sent += sum(counts)
         inbox = recv
-    return ShardedResult(backend.local_dist(), steps, sent)
+    return ShardedResult(backend.local_dist(), steps, sent, _backend_ms(backend), clk.ms)
 
 
 def solve_logical(backends: Sequence, source: int, max_steps: int = 1 << 20) -> ShardedResult:
@@ -189,12 +221,14 @@ def solve_logical(backends: Sequence, source: int, max_steps: int = 1 << 20) -> 
         b.begin()
     inboxes = [_source_inbox(b, source, P, r) for r, b in enumerate(backends)]
     steps = sent = 0
+    clk = _Clock(backends[0].device)
     while steps < max_steps:
         outs = [b.step(inboxes[r]) for r, b in enumerate(backends)]
         steps += 1
         total = sum(sum(c) for _, c in outs)
         if total == 0:
             break
+        clk.start()
         sent += total
         nxt = []
         for dst in range(P):
@@ -204,8 +238,10 @@ def solve_logical(backends: Sequence, source: int, max_steps: int = 1 << 20) -> 
                 parts.append(send[lo: lo + 2 * counts[dst]].to(backends[dst].device))
             nxt.append(torch.cat(parts) if parts else backends[dst].empty_inbox())
         inboxes = nxt
-    n = sum(b.local_dist().size for b in backends)
-    return ShardedResult(merge_local([b.local_dist() for b in backends], n), steps, sent)
+        clk.stop()
+    dists = [b.local_dist() for b in backends]
+    n = sum(d.size for d in dists)
+    return ShardedResult(merge_local(dists, n), steps, sent, sum(_backend_ms(b) for b in backends), clk.ms)
 
 
 def sssp_solve_sharded(graph: CsrGraph, source: int, nparts: int, config: Optional[MlmqConfig] = None,

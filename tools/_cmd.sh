@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_sharded.py -x -q -m gpu > gpurun_out/pytest_shard.log 2>&1; echo pytest=$? >> gpurun_out/pytest_shard.log
-for P in 1 2 4 8; do timeout 300 python tools/shard_repro.py $P 20 >> gpurun_out/shard_s20.log 2>&1; done
+for P in 2 4 8; do timeout 600 python bench.py --config c2 --parts $P --steps 3 --warmup 2 --no-cpu > gpurun_out/bench_c2_p$P.log 2>&1; done
+timeout 1500 python bench.py --config c4 --parts 8 --steps 2 --warmup 1 --no-cpu > gpurun_out/bench_c4_p8.log 2>&1
