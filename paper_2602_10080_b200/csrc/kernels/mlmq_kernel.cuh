@@ -20,7 +20,7 @@
 
 namespace mlmq {
 
-template <int K, int L2K, int CM>
+template <int K, int L2K, int CM, int L1T>
 struct Worker {
   using Tr = DT<K>;
   using S = typename Tr::S;
@@ -71,7 +71,7 @@ struct Worker {
     spill = outs + p.out_cap;
     l1a = spill + p.spill_cap;
     l1b = l1a + p.l1cap;
-    const int l1n = (p.l1type == L1K_NEAR_FAR ? 2 : 1) * p.l1cap;
+    const int l1n = (L1T == L1K_NEAR_FAR ? 2 : 1) * p.l1cap;
     fars = l1a + l1n;  // far staging (bucket window), p.far_cap elements
     met = reinterpret_cast<unsigned long long*>(fars + p.far_cap);
     met[lane] = 0;  // metric + profile slots (kMetSlots == 32)
@@ -82,7 +82,7 @@ struct Worker {
     l0n = 0;
     wc = rc = l0size = 0;
     h1 = n1 = h2 = n2 = 0;
-    thr = (S)(p.l1type == L1K_NEAR_FAR ? p.delta_nf_s : p.filter_f_s);
+    thr = (S)(L1T == L1K_NEAR_FAR ? p.delta_nf_s : p.filter_f_s);
     rej_min = (S)Tr::INF;
     has_rej = false;
     wcount = 0;
@@ -1158,7 +1158,7 @@ struct Worker {
 
   __device__ void l1_write(int ns) {
     LOC();
-    switch (p.l1type) {
+    switch (L1T) {
       case L1K_VECTOR: l1_vector_write(ns); break;
       case L1K_NEAR_FAR: l1_nearfar_write(ns); break;
       case L1K_FILTER: l1_filter_write(ns); break;
@@ -1171,7 +1171,7 @@ struct Worker {
     LOC();
     loc(12);
     const int cap = p.l1cap;
-    if (p.l1type == L1K_NEAR_FAR) {
+    if (L1T == L1K_NEAR_FAR) {
       if (n1 == 0 && n2 > 0) {
         S mn = (S)Tr::INF;
         for (int i = lane; i < n2; i += 32) {
@@ -1208,7 +1208,7 @@ struct Worker {
       }
       return ring_pop_front(l1a, h1, n1, dst, want);
     }
-    if (p.l1type == L1K_FILTER && n1 == 0) {
+    if (L1T == L1K_FILTER && n1 == 0) {
       if (has_rej) {
         thr = Tr::add_thr(rej_min, (S)p.filter_f_s);
         rej_min = (S)Tr::INF;
@@ -1882,8 +1882,8 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
   }
 }
 
-template <int K, int L2K, int CM>
-__global__ void __launch_bounds__(256) mlmq_persistent_kernel(const __grid_constant__ KParams p) {
+template <int K, int L2K, int CM, int L1T>
+__global__ void __launch_bounds__(256, 2) mlmq_persistent_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -1893,7 +1893,7 @@ __global__ void __launch_bounds__(256) mlmq_persistent_kernel(const __grid_const
     if ((kDebug && p.wstate) && lane == 0) p.wstate[2 * (size_t)p.G + 4] = 2;
     return;
   }
-  Worker<K, L2K, CM> w(p, smem + (size_t)warp * p.smem_per_warp, gid, lane);
+  Worker<K, L2K, CM, L1T> w(p, smem + (size_t)warp * p.smem_per_warp, gid, lane);
   w.run();
 }
 

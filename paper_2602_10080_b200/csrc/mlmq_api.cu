@@ -25,24 +25,78 @@
 
 namespace mlmq {
 
-const void* kernel_dk0_l0_c4();
-const void* kernel_dk0_l0_c16();
-const void* kernel_dk0_l1_c4();
-const void* kernel_dk0_l1_c16();
-const void* kernel_dk0_l2_c4();
-const void* kernel_dk0_l2_c16();
-const void* kernel_dk1_l0_c4();
-const void* kernel_dk1_l0_c16();
-const void* kernel_dk1_l1_c4();
-const void* kernel_dk1_l1_c16();
-const void* kernel_dk1_l2_c4();
-const void* kernel_dk1_l2_c16();
-const void* kernel_dk2_l0_c4();
-const void* kernel_dk2_l0_c16();
-const void* kernel_dk2_l1_c4();
-const void* kernel_dk2_l1_c16();
-const void* kernel_dk2_l2_c4();
-const void* kernel_dk2_l2_c16();
+const void* kernel_dk0_l0_c4_q0();
+const void* kernel_dk0_l0_c4_q1();
+const void* kernel_dk0_l0_c4_q2();
+const void* kernel_dk0_l0_c4_q3();
+const void* kernel_dk0_l0_c16_q0();
+const void* kernel_dk0_l0_c16_q1();
+const void* kernel_dk0_l0_c16_q2();
+const void* kernel_dk0_l0_c16_q3();
+const void* kernel_dk0_l1_c4_q0();
+const void* kernel_dk0_l1_c4_q1();
+const void* kernel_dk0_l1_c4_q2();
+const void* kernel_dk0_l1_c4_q3();
+const void* kernel_dk0_l1_c16_q0();
+const void* kernel_dk0_l1_c16_q1();
+const void* kernel_dk0_l1_c16_q2();
+const void* kernel_dk0_l1_c16_q3();
+const void* kernel_dk0_l2_c4_q0();
+const void* kernel_dk0_l2_c4_q1();
+const void* kernel_dk0_l2_c4_q2();
+const void* kernel_dk0_l2_c4_q3();
+const void* kernel_dk0_l2_c16_q0();
+const void* kernel_dk0_l2_c16_q1();
+const void* kernel_dk0_l2_c16_q2();
+const void* kernel_dk0_l2_c16_q3();
+const void* kernel_dk1_l0_c4_q0();
+const void* kernel_dk1_l0_c4_q1();
+const void* kernel_dk1_l0_c4_q2();
+const void* kernel_dk1_l0_c4_q3();
+const void* kernel_dk1_l0_c16_q0();
+const void* kernel_dk1_l0_c16_q1();
+const void* kernel_dk1_l0_c16_q2();
+const void* kernel_dk1_l0_c16_q3();
+const void* kernel_dk1_l1_c4_q0();
+const void* kernel_dk1_l1_c4_q1();
+const void* kernel_dk1_l1_c4_q2();
+const void* kernel_dk1_l1_c4_q3();
+const void* kernel_dk1_l1_c16_q0();
+const void* kernel_dk1_l1_c16_q1();
+const void* kernel_dk1_l1_c16_q2();
+const void* kernel_dk1_l1_c16_q3();
+const void* kernel_dk1_l2_c4_q0();
+const void* kernel_dk1_l2_c4_q1();
+const void* kernel_dk1_l2_c4_q2();
+const void* kernel_dk1_l2_c4_q3();
+const void* kernel_dk1_l2_c16_q0();
+const void* kernel_dk1_l2_c16_q1();
+const void* kernel_dk1_l2_c16_q2();
+const void* kernel_dk1_l2_c16_q3();
+const void* kernel_dk2_l0_c4_q0();
+const void* kernel_dk2_l0_c4_q1();
+const void* kernel_dk2_l0_c4_q2();
+const void* kernel_dk2_l0_c4_q3();
+const void* kernel_dk2_l0_c16_q0();
+const void* kernel_dk2_l0_c16_q1();
+const void* kernel_dk2_l0_c16_q2();
+const void* kernel_dk2_l0_c16_q3();
+const void* kernel_dk2_l1_c4_q0();
+const void* kernel_dk2_l1_c4_q1();
+const void* kernel_dk2_l1_c4_q2();
+const void* kernel_dk2_l1_c4_q3();
+const void* kernel_dk2_l1_c16_q0();
+const void* kernel_dk2_l1_c16_q1();
+const void* kernel_dk2_l1_c16_q2();
+const void* kernel_dk2_l1_c16_q3();
+const void* kernel_dk2_l2_c4_q0();
+const void* kernel_dk2_l2_c4_q1();
+const void* kernel_dk2_l2_c4_q2();
+const void* kernel_dk2_l2_c4_q3();
+const void* kernel_dk2_l2_c16_q0();
+const void* kernel_dk2_l2_c16_q1();
+const void* kernel_dk2_l2_c16_q2();
+const void* kernel_dk2_l2_c16_q3();
 
 static thread_local char g_err[1024] = "";
 
@@ -165,13 +219,13 @@ struct ShardIo {
 
 namespace {
 
-const void* kernel_for(int dk, int l2k, int cm) {
+const void* kernel_for(int dk, int l2k, int cm, int l1) {
   using Fn = const void* (*)();
-  static const Fn table[3][3][2] = {
-    {{kernel_dk0_l0_c4, kernel_dk0_l0_c16}, {kernel_dk0_l1_c4, kernel_dk0_l1_c16}, {kernel_dk0_l2_c4, kernel_dk0_l2_c16}},
-    {{kernel_dk1_l0_c4, kernel_dk1_l0_c16}, {kernel_dk1_l1_c4, kernel_dk1_l1_c16}, {kernel_dk1_l2_c4, kernel_dk1_l2_c16}},
-    {{kernel_dk2_l0_c4, kernel_dk2_l0_c16}, {kernel_dk2_l1_c4, kernel_dk2_l1_c16}, {kernel_dk2_l2_c4, kernel_dk2_l2_c16}}};
-  return table[dk][l2k][cm <= 4 ? 0 : 1]();
+  static const Fn table[3][3][2][4] = {
+    {{{kernel_dk0_l0_c4_q0, kernel_dk0_l0_c4_q1, kernel_dk0_l0_c4_q2, kernel_dk0_l0_c4_q3}, {kernel_dk0_l0_c16_q0, kernel_dk0_l0_c16_q1, kernel_dk0_l0_c16_q2, kernel_dk0_l0_c16_q3}}, {{kernel_dk0_l1_c4_q0, kernel_dk0_l1_c4_q1, kernel_dk0_l1_c4_q2, kernel_dk0_l1_c4_q3}, {kernel_dk0_l1_c16_q0, kernel_dk0_l1_c16_q1, kernel_dk0_l1_c16_q2, kernel_dk0_l1_c16_q3}}, {{kernel_dk0_l2_c4_q0, kernel_dk0_l2_c4_q1, kernel_dk0_l2_c4_q2, kernel_dk0_l2_c4_q3}, {kernel_dk0_l2_c16_q0, kernel_dk0_l2_c16_q1, kernel_dk0_l2_c16_q2, kernel_dk0_l2_c16_q3}}},
+    {{{kernel_dk1_l0_c4_q0, kernel_dk1_l0_c4_q1, kernel_dk1_l0_c4_q2, kernel_dk1_l0_c4_q3}, {kernel_dk1_l0_c16_q0, kernel_dk1_l0_c16_q1, kernel_dk1_l0_c16_q2, kernel_dk1_l0_c16_q3}}, {{kernel_dk1_l1_c4_q0, kernel_dk1_l1_c4_q1, kernel_dk1_l1_c4_q2, kernel_dk1_l1_c4_q3}, {kernel_dk1_l1_c16_q0, kernel_dk1_l1_c16_q1, kernel_dk1_l1_c16_q2, kernel_dk1_l1_c16_q3}}, {{kernel_dk1_l2_c4_q0, kernel_dk1_l2_c4_q1, kernel_dk1_l2_c4_q2, kernel_dk1_l2_c4_q3}, {kernel_dk1_l2_c16_q0, kernel_dk1_l2_c16_q1, kernel_dk1_l2_c16_q2, kernel_dk1_l2_c16_q3}}},
+    {{{kernel_dk2_l0_c4_q0, kernel_dk2_l0_c4_q1, kernel_dk2_l0_c4_q2, kernel_dk2_l0_c4_q3}, {kernel_dk2_l0_c16_q0, kernel_dk2_l0_c16_q1, kernel_dk2_l0_c16_q2, kernel_dk2_l0_c16_q3}}, {{kernel_dk2_l1_c4_q0, kernel_dk2_l1_c4_q1, kernel_dk2_l1_c4_q2, kernel_dk2_l1_c4_q3}, {kernel_dk2_l1_c16_q0, kernel_dk2_l1_c16_q1, kernel_dk2_l1_c16_q2, kernel_dk2_l1_c16_q3}}, {{kernel_dk2_l2_c4_q0, kernel_dk2_l2_c4_q1, kernel_dk2_l2_c4_q2, kernel_dk2_l2_c4_q3}, {kernel_dk2_l2_c16_q0, kernel_dk2_l2_c16_q1, kernel_dk2_l2_c16_q2, kernel_dk2_l2_c16_q3}}}};
+  return table[dk][l2k][cm <= 4 ? 0 : 1][l1]();
 }
 
 int l2_kind(int l2_type) {
@@ -212,7 +266,7 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
   s->dk = dk;
   s->l2k = l2_kind(c->l2_type);
   s->cm = c->l0_capacity <= 4 ? 4 : 16;
-  s->fn = kernel_for(dk, s->l2k, s->cm);
+  s->fn = kernel_for(dk, s->l2k, s->cm, c->l1_type);
   const int es = dk == DK_U64 ? 16 : 8;
   const int L = c->lanes_per_group;
   s->batch_cap = std::max(c->block_size, 32);

@@ -290,3 +290,35 @@ def test_random_sources_and_configs_fuzz():
         want = oracle_dist(g, s)
         assert compare_distances(r.dist_array, want) is None, (trial, cfg)
         assert_balanced(r.metrics)
+
+
+@pytest.mark.parametrize("win", [0, 1, 2, 4])
+def test_bucket_window_managed_floor_exact(win):
+    # B200 extension: winners >= win buckets above the floor bypass L0/L1 and the manager
+    # advances the floor only when the near window is quiescent (Delta-stepping order)
+    graphs = [generate_grid2d(64, 64, 1, 100, seed=1),
+              generate_graph("rmat", seed=3, scale=12, edge_factor=16, wmin=1, wmax=255),
+              generate_graph("path", seed=2, n=3000, wmin=1, wmax=9)]
+    for g in graphs:
+        f = extract_features(g)
+        want = oracle_dist(g)
+        for l1 in ("vector", "near_far", "filter", "slf"):
+            for ds, groups in ((1, None), (4, 64), (0.5, 3)):
+                aw = max(1, round(f.avg_weight))
+                cfg = MlmqConfig(l1_type=l1, l2_type="bucket", l1_params=L1Params(capacity=256),
+                                 l2_params=L2Params(delta=max(1, int(ds * aw)), bmax=64),
+                                 num_groups=groups)
+                r = sssp_solve(g, 0, cfg, EngineConfig(bucket_window=win), features=f)
+                assert np.array_equal(r.dist_array, want), (l1, ds, groups)
+                assert_balanced(r.metrics)
+
+
+def test_bucket_window_small_rings_spill_over_not_overflow():
+    # far buckets overfill small rings: writers move on to farther rings instead of
+    # wedging on a full one (occupancy-aware placement)
+    g = generate_graph("rmat", seed=1, scale=14, edge_factor=16, wmin=1, wmax=255)
+    cfg = MlmqConfig(l1_type="vector", l2_type="bucket",
+                     l2_params=L2Params(delta=128, bmax=8, block_size=16, block_num=64),
+                     num_groups=None)
+    r = sssp_solve(g, 0, cfg, EngineConfig(bucket_window=1, spin_timeout_s=10))
+    assert np.array_equal(r.dist_array, oracle_dist(g))
