@@ -150,6 +150,11 @@ int mlmq_sssp_f32(mlmq_graph* g, uint64_t source, const mlmq_config_t* cfg,
 int mlmq_sssp_device(mlmq_graph* g, uint64_t source, const mlmq_config_t* cfg,
                      mlmq_metrics_t* metrics_out);
 
+/* Page-locked host memory for result buffers: D2H into it runs at full PCIe/C2C speed
+ * (the Python shim recycles these buffers across solves). */
+int mlmq_host_alloc(uint64_t bytes, void** out);
+void mlmq_host_free(void* p);
+
 /* Copy the last solve's device distances (as stored: u32/u64 words) to the host. */
 int mlmq_last_dist(mlmq_graph* g, uint64_t* dist_out);
 

@@ -74,6 +74,7 @@ EXPORTED_SYMBOLS = (
     "mlmq_sssp", "mlmq_sssp_f32", "mlmq_sssp_device", "mlmq_last_dist", "mlmq_reach",
     "mlmq_feature_sums", "mlmq_gen_size", "mlmq_gen_graph", "mlmq_build_csr",
     "mlmq_gen_f32_weights", "mlmq_shard_create", "mlmq_shard_begin", "mlmq_shard_step",
+    "mlmq_host_alloc", "mlmq_host_free",
 )
 
 _lib = None
@@ -119,6 +120,8 @@ def lib():
             "mlmq_shard_create": ([P, P, P, I32, U64, U64, U64, ctypes.c_uint32, ctypes.c_uint32, I32, P], I32),
             "mlmq_shard_begin": ([P], I32),
             "mlmq_shard_step": ([P, P, P, U64, P, U64, P, P], I32),
+            "mlmq_host_alloc": ([U64, P], I32),
+            "mlmq_host_free": ([P], None),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -150,6 +153,54 @@ def device_count() -> int:
     n = ctypes.c_int(0)
     lib().mlmq_device_count(ctypes.byref(n))
     return int(n.value)
+
+
+class _PinnedBlock:
+    """Owner of one page-locked host buffer; returns it to the pool when the last numpy
+    array viewing it is garbage collected."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr, self.nbytes = ptr, nbytes
+
+    def __del__(self):
+        try:
+            _pinned_release(self)
+        except Exception:
+            pass
+
+
+_pool_lock = threading.Lock()
+_pool: dict = {}
+_POOL_MAX_PER_SIZE = 4
+
+
+def _pinned_release(block: _PinnedBlock) -> None:
+    with _pool_lock:
+        free = _pool.setdefault(block.nbytes, [])
+        if len(free) < _POOL_MAX_PER_SIZE:
+            free.append(block.ptr)
+            return
+    lib().mlmq_host_free(block.ptr)
+
+
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """np.empty(n, dtype) in page-locked memory, recycled across solves (result buffers
+    for device->host copies at full link speed)."""
+    dt = np.dtype(dtype)
+    nbytes = max(64, int(n) * dt.itemsize)
+    ptr = None
+    with _pool_lock:
+        free = _pool.get(nbytes)
+        if free:
+            ptr = free.pop()
+    if ptr is None:
+        p = ctypes.c_void_p()
+        check(lib().mlmq_host_alloc(nbytes, ctypes.byref(p)))
+        ptr = p.value
+    block = _PinnedBlock(ptr, nbytes)
+    buf = (ctypes.c_char * nbytes).from_address(ptr)
+    buf._mlmq_block = block  # the ctypes buffer keeps the owner alive; numpy keeps the buffer
+    return np.frombuffer(buf, dtype=dt, count=int(n))
 
 
 def _ptr(a: Optional[np.ndarray]):
@@ -201,11 +252,11 @@ class DeviceGraph:
         m = Metrics()
         gm = np.zeros((max(want_groups, 1), GROUP_METRIC_FIELDS), dtype=np.uint64)
         if self.weight_kind == W_F32:
-            dist = np.empty(self.n, dtype=np.float32)
+            dist = pinned_empty(self.n, np.float32)
             st = self._lib.mlmq_sssp_f32(self.handle, source, ctypes.byref(cfg), _ptr(dist),
                                          ctypes.byref(m), _ptr(gm), want_groups)
         else:
-            dist = np.empty(self.n, dtype=np.uint64)
+            dist = pinned_empty(self.n, np.uint64)
             st = self._lib.mlmq_sssp(self.handle, source, ctypes.byref(cfg), _ptr(dist),
                                      ctypes.byref(m), _ptr(gm), want_groups)
         check(st)

@@ -1032,6 +1032,17 @@ int mlmq_reach(mlmq_graph* g, uint64_t* v_reach, uint64_t* e_reach) {
   return MLMQ_OK;
 }
 
+int mlmq_host_alloc(uint64_t bytes, void** out) {
+  if (!out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  *out = nullptr;
+  CK(cudaHostAlloc(out, std::max<uint64_t>(bytes, 64), cudaHostAllocPortable));
+  return MLMQ_OK;
+}
+
+void mlmq_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int mlmq_shard_create(const uint64_t* row_offsets, const uint32_t* col, const void* w, int weight_kind,
                       uint64_t n_local, uint64_t m_local, uint64_t n_global, uint32_t rank, uint32_t nparts,
                       int device, mlmq_graph** out) {
