@@ -58,6 +58,7 @@ struct Worker {
   unsigned n_relax, n_upd;  // relaxations (per lane) / distance updates (warp), folded at exit
   int mcursor;
   int outn;
+  int nfar;  // far elements staged (bucket window)
   bool dist_ovf;
   bool idle;
   int last_src;  // level that served the current batch (1 L0, 2 L1, 3 L2) for diagnostics
@@ -90,6 +91,7 @@ struct Worker {
     n_relax = n_upd = 0;
     mcursor = p.pnum > 0 ? gid % p.pnum : 0;
     outn = 0;
+    nfar = 0;
     dist_ovf = false;
     pend = ~0ull;
     idle = false;
@@ -163,6 +165,11 @@ struct Worker {
   // Work generation (B200 extension): bumped after every publication of new shared work
   // (ring block, hub descriptor, heap node, floor advance).  An idle group polls this
   // one word (with the stop flag beside it) instead of re-walking the whole cascade.
+  // managed floor: is ring rid the head or the ring behind it (claimable by readers)?
+  __device__ __forceinline__ bool near_ring(int rid, int emod) const {
+    const int rel = rid >= emod ? rid - emod : rid + p.bmax - emod;
+    return rel == 0 || rel == p.bmax - 1;
+  }
   __device__ __forceinline__ void bump_gen() const {
     if (lane == 0) red_add(p.ctl + C_GEN, 1ull);
   }
@@ -325,7 +332,12 @@ struct Worker {
       st_release(p.seq + i, tk + 1);
     }
     __syncwarp();
-    bump_gen();
+    if (L2K == L2K_BUCKET && p.bwin > 0) {  // warp-uniform here
+      const int emod = (int)(warp_ld(p.ctl + C_EPOCH) % (unsigned long long)p.bmax);
+      if (near_ring(rid, emod)) bump_gen();
+    } else {
+      bump_gen();
+    }
   }
 
   // Writer (l2.py:96-114): one fetch-add claims ceil(n/bs) tickets; all slot waits,
@@ -543,32 +555,49 @@ struct Worker {
     // `ring_margin` of capacity) passes its elements on to the next ring.  Any ring is a
     // correct home (the reader rebins or processes them), so a burst of far work can no
     // longer wedge a writer on a full ring while the floor waits for near work.
+    const long long room = (long long)(p.bn_mask + 1) - p.ring_margin;
     for (int b = lane; b < p.bmax; b += 32) {
-      const unsigned long long occ = ld_relaxed(wp(b)) - ld_relaxed(rp(b));
-      bcur[b] = (long long)occ > (long long)(p.bn_mask + 1) - p.ring_margin ? 1u : 0u;
       bhist[b] = 0;
+      bcur[b] = 0;
+      bremap[b] = b;
     }
-    __syncwarp();
-    for (int b = lane; b < p.bmax; b += 32) {
-      // move only farther from the floor and never past the clamp ring: an element is
-      // never placed where it would be rebinned straight back (no livelock)
-      int t = b;
-      int rel = b >= emod ? b - emod : b + p.bmax - emod;
-      while (bcur[t] && rel > 0 && rel < rel_clamp()) {
-        t = t + 1 == p.bmax ? 0 : t + 1;
-        ++rel;
-      }
-      bremap[b] = bcur[t] ? b : t;  // no room anywhere farther: keep the home ring (bounded wait)
-    }
-    __syncwarp();
-    for (int b = lane; b < p.bmax; b += 32) bcur[b] = 0;
     __syncwarp();
     for (int i = lane; i < n; i += 32) {
       LOC();
       const E x = base[(unsigned)(start + i) % (unsigned)cap];
-      atomicAdd(bhist + bremap[bring(emod, bucket_rel(x.d, e))], 1u);
+      atomicAdd(bhist + bring(emod, bucket_rel(x.d, e)), 1u);
     }
     __syncwarp();
+    bool anyfull = false;  // occupancy of the rings this write uses (one load pair each)
+    for (int b = lane; b < p.bmax; b += 32)
+      if (bhist[b]) anyfull |= (long long)(ld_relaxed(wp(b)) - ld_relaxed(rp(b))) > room;
+    if (__any_sync(FULL, anyfull)) {
+      for (int b = lane; b < p.bmax; b += 32)
+        bcur[b] = (long long)(ld_relaxed(wp(b)) - ld_relaxed(rp(b))) > room ? 1u : 0u;
+      __syncwarp();
+      for (int b = lane; b < p.bmax; b += 32) {
+        // move only farther from the floor and never past the clamp ring: an element is
+        // never placed where it would be rebinned straight back (no livelock)
+        int t = b;
+        int rel = b >= emod ? b - emod : b + p.bmax - emod;
+        while (bcur[t] && rel > 0 && rel < rel_clamp()) {
+          t = t + 1 == p.bmax ? 0 : t + 1;
+          ++rel;
+        }
+        bremap[b] = bcur[t] ? b : t;  // no room anywhere farther: keep the home ring (bounded wait)
+      }
+      __syncwarp();
+      for (int b = lane; b < p.bmax; b += 32) {
+        bcur[b] = 0;
+        bhist[b] = 0;
+      }
+      __syncwarp();
+      for (int i = lane; i < n; i += 32) {
+        const E x = base[(unsigned)(start + i) % (unsigned)cap];
+        atomicAdd(bhist + bremap[bring(emod, bucket_rel(x.d, e))], 1u);
+      }
+      __syncwarp();
+    }
     int used = 0;
     for (int b = lane; b < p.bmax; b += 32) {
       LOC();
@@ -617,7 +646,11 @@ struct Worker {
       }
     }
     __syncwarp();
-    bump_gen();
+    // managed floor: only blocks in the head / behind rings are claimable now, so only
+    // they wake idle groups (far rings wait for the manager's floor advance, which bumps)
+    bool wake = !(p.bwin > 0);
+    for (int b = lane; b < p.bmax; b += 32) wake |= bhist[b] && near_ring(b, emod);
+    if (__any_sync(FULL, wake)) bump_gen();
   }
 
   // l2.py:235-295: scan bnum buckets from the floor; rebin stale-slot elements; advance
@@ -1266,11 +1299,18 @@ struct Worker {
   // bwin or more buckets above the current floor bypass the group-private L0/L1 and go
   // straight to their L2 bucket, so the private levels only ever hold near-floor work
   // and thousands of groups cannot run far ahead of the floor (work inflation).
+  __device__ void far_flush() {
+    if (nfar > 0) write_back(fars, 0, nfar, LINEAR);
+    nfar = 0;
+  }
   __device__ void far_split() {
+    // The floor cannot move while this group holds work (its unflushed done count keeps
+    // the near window busy), so far elements are staged across flushes and written as
+    // full, bucket-grouped blocks when the stage fills or the group runs out of work.
     const unsigned long long e = warp_ld(p.ctl + C_EPOCH);
-    const int emod = (int)(e % (unsigned long long)p.bmax);
-    int kept = 0, nfar = 0;
+    int kept = 0;
     for (int o = 0; o < outn; o += 32) {
+      if (nfar + 32 > p.far_cap) far_flush();
       const bool has = o + lane < outn;
       E x = E();
       int rel = 0;
@@ -1290,8 +1330,6 @@ struct Worker {
       __syncwarp();
     }
     outn = kept;
-    // one histogram-grouped write: one ticket and full blocks per target bucket
-    if (nfar > 0) write_back(fars, 0, nfar, LINEAR);
   }
 
   __device__ void flush_out(bool all) {
@@ -1768,6 +1806,7 @@ struct Worker {
         backoff = 0;
         continue;
       }
+      if (L2K == L2K_BUCKET && nfar > 0) far_flush();  // staged far work leaves before idling
       if (!idle) {
         idle = true;
         seen = ~0ull;  // the first miss re-checks once against a generation read before it
@@ -1805,7 +1844,8 @@ struct Worker {
       for (int f = 0; f < M_COUNT; ++f) p.metrics[(size_t)gid * M_COUNT + f] = met[f];
       if (kDebug && p.prof)
         for (int f = 0; f < P_COUNT; ++f) p.prof[(size_t)gid * P_COUNT + f] = met[kProfBase + f];
-      if (l0size + l1size + outn) atomicAdd(p.ctl + C_LOCAL_NONEMPTY, (unsigned long long)(l0size + l1size + outn));
+      if (l0size + l1size + outn + nfar)
+        atomicAdd(p.ctl + C_LOCAL_NONEMPTY, (unsigned long long)(l0size + l1size + outn + nfar));
     }
   }
 };
@@ -1814,8 +1854,9 @@ struct Worker {
 static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
   int k = 0, kq = 0;
   if ((kDebug && p.wstate) && lane == 0) p.wstate[2 * (size_t)p.G + 4] = 1;
-  for (;;) {
-    if (p.host_abort && lane == 0 && ld_sys_u32(p.host_abort) != 0u) {
+  for (int it = 0;; ++it) {
+    // the abort word lives in host memory (a PCIe round trip): poll it every 32 iterations
+    if (p.host_abort && lane == 0 && (it & 31) == 0 && ld_sys_u32(p.host_abort) != 0u) {
       atomicCAS(p.ctl + C_ERR, 0ull, (unsigned long long)ERR_ABORT);
       __threadfence();
       st_release(p.ctl + C_STOP, 1ull);
@@ -1863,6 +1904,12 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
         if (lane == 0) {
           st_release(p.ctl + C_EPOCH, e + (unsigned long long)first);
           red_add(p.ctl + C_GEN, 1ull);
+          if (kDebug && p.wstate) {  // epoch log for the debug dump
+            unsigned long long* E = p.wstate + 2 * (size_t)p.G + 8 + (size_t)p.G * 32;
+            const unsigned long long i = ++E[0];
+            const unsigned long long busy = (unsigned long long)p.G - ld_relaxed(p.ctl + C_IDLE);
+            if (i < 8192) E[i] = (globaltimer_ns() << 16) | (busy & 0xFFFF);
+          }
         }
         kq = 0;
       }

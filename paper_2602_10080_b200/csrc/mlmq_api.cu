@@ -406,7 +406,7 @@ bool debug_enabled() {
 
 // MLMQ_DEBUG=1: per-phase cycle breakdown and the wait states of stuck warps.
 void debug_dump(mlmq_graph* g, int G, const char* tag) {
-  std::vector<unsigned long long> pr((size_t)G * P_COUNT), ws((size_t)2 * G + 8 + (size_t)G * 32);
+  std::vector<unsigned long long> pr((size_t)G * P_COUNT), ws((size_t)2 * G + 8 + (size_t)G * 32 + 8192);
   std::vector<unsigned long long> ctl(C_WORDS), ptr(64);
   if (cudaMemcpy(pr.data(), g->d_prof, pr.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
       cudaMemcpy(ws.data(), g->d_wstate, ws.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
@@ -471,6 +471,23 @@ void debug_dump(mlmq_graph* g, int G, const char* tag) {
       }
     }
   }
+  {  // managed-floor epoch log: [0] count, then (timestamp << 16 | busy groups) per advance
+    const unsigned long long* E = &ws[(size_t)2 * G + 8 + (size_t)G * 32];
+    const unsigned long long ne = std::min<unsigned long long>(E[0], 8191);
+    if (ne > 1) {
+      std::vector<double> d;
+      double busy = 0;
+      for (unsigned long long i = 2; i <= ne; ++i) {
+        d.push_back(((E[i] >> 16) - (E[i - 1] >> 16)) / 1e3);
+        busy += (double)(E[i] & 0xFFFF);
+      }
+      std::sort(d.begin(), d.end());
+      double s = 0;
+      for (double x : d) s += x;
+      fprintf(stderr, "[mlmq debug]   epochs %llu: gap us mean %.2f median %.2f p90 %.2f max %.2f; busy groups at advance %.1f\n",
+              ne, s / d.size(), d[d.size() / 2], d[d.size() * 9 / 10], d.back(), busy / (ne - 1));
+    }
+  }
   fprintf(stderr, "[mlmq debug]   phases:");
   for (int i = 0; i < 128; ++i)
     if (lh[i]) fprintf(stderr, " %d:%d", i, lh[i]);
@@ -504,12 +521,12 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     cudaFree(g->d_prof);
     cudaFree(g->d_wstate);
     CK(cudaMalloc(&g->d_prof, (size_t)G * P_COUNT * 8));
-    CK(cudaMalloc(&g->d_wstate, (size_t)G * 16 + 64 + (size_t)G * 256));
+    CK(cudaMalloc(&g->d_wstate, (size_t)G * 16 + 64 + (size_t)G * 256 + 8 * 8192));
     g->prof_cap = G;
   }
   if (dbg) {
     CK(cudaMemset(g->d_prof, 0, (size_t)G * P_COUNT * 8));
-    CK(cudaMemset(g->d_wstate, 0, (size_t)G * 16 + 64 + (size_t)G * 256));
+    CK(cudaMemset(g->d_wstate, 0, (size_t)G * 16 + 64 + (size_t)G * 256 + 8 * 8192));
   }
   KParams p;
   std::memset(&p, 0, sizeof(p));
