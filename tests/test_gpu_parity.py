@@ -322,3 +322,41 @@ def test_bucket_window_small_rings_spill_over_not_overflow():
                      num_groups=None)
     r = sssp_solve(g, 0, cfg, EngineConfig(bucket_window=1, spin_timeout_s=10))
     assert np.array_equal(r.dist_array, oracle_dist(g))
+
+
+# ------------------------------------------------------------------ BASELINE configs
+C2_DIST = "f6d20099af4ad32ebcc888faa9f557f17b69be966c4c0808093799b5f3840788"
+C3_DIST = "2bf8e0cf2ab0c6ab8b906952288c22c564fbda5404ab78d48e8c90590c3bde41"
+
+
+@pytest.mark.parametrize("name,sha", [("c1", C1_DIST), ("c2", C2_DIST), ("c3", C3_DIST)])
+def test_baseline_configs_match_reference_hashes(name, sha):
+    # the bench's own engine configurations on the BASELINE graphs, against the
+    # reference dijkstra_oracle's dist_sha256 (produced by the reference)
+    from bench import build_graph, solve_config
+    g = build_graph(name)
+    f = extract_features(g)
+    for _ in range(2):
+        r = sssp_solve(g, 0, solve_config(name, g, f), EngineConfig(bucket_window=1), features=f)
+        assert oracle.dist_sha256(r.dist_array) == sha
+        assert_balanced(r.metrics)
+
+
+def test_c5_float_weights_match_f32_oracle():
+    from bench import build_graph, solve_config
+    g = build_graph("c5")
+    f = extract_features(g)
+    r = sssp_solve(g, 0, solve_config("c5", g, f), features=f)
+    want = oracle.dijkstra_f32(g.row_offsets, g.col_indices, g.weights, 0)
+    assert np.array_equal(r.dist_array, want)
+
+
+def test_sharded_equals_unsharded_on_c2():
+    from bench import build_graph, solve_config
+    from paper_2602_10080_b200.sharded import sssp_solve_sharded
+    g = build_graph("c2")
+    f = extract_features(g)
+    want = sssp_solve(g, 0, solve_config("c2", g, f), features=f).dist_array
+    for P in (2, 8):
+        res = sssp_solve_sharded(g, 0, P, MlmqConfig(l2_type="fifo"))
+        assert np.array_equal(res.local_dist, want), P
