@@ -292,6 +292,7 @@ struct KParams {
   int bwin;                     // bucket window: winners >= bwin buckets above the floor skip L0/L1 (0 = off)
   int batch_cap, out_cap, spill_cap;  // elements
   int far_cap;                  // far staging elements (bucket window), 0 when unused
+  int l1_want;                  // elements per L1 read (reference: lanes_per_group)
   long long ring_margin;        // bucket rings: pending blocks kept free for racing writers
 
   // 1D-partitioned shard; nparts == 1 for an unpartitioned graph

@@ -1734,7 +1734,7 @@ struct Worker {
       return c;
     }
     last_src = 2;
-    const int c1 = l1_read(batch, L);
+    const int c1 = l1_read(batch, p.l1_want);
     pacc(P_L0L1, t0);
     if (c1 > 0) {
       count(M_L1D, (unsigned long long)c1);

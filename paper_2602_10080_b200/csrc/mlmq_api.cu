@@ -597,6 +597,10 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.out_cap = kOutCap;
   p.spill_cap = sh.spill_cap;
   p.far_cap = sh.far_cap;
+  {
+    const char* w = getenv("MLMQ_L1_WANT");  // experiment knob
+    p.l1_want = std::max(1, std::min(w ? atoi(w) : c->lanes_per_group, sh.batch_cap));
+  }
   p.ring_margin = std::min<long long>((long long)w.bn / 2, 4LL * G + 64);
   p.share = c->share ? 1 : 0;
   p.fifo_park = (sh.l2k == L2K_FIFO && c->fifo_park) ? 1 : 0;

@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/pytest_gpu.log
+mkdir -p gpurun_out/selector
+timeout 2400 python tools/selector_sweep.py gpurun_out/selector > gpurun_out/selector/sweep.log 2>&1; echo rc=$? >> gpurun_out/selector/sweep.log
