@@ -84,7 +84,9 @@ typedef struct {
   int32_t fifo_park;                /* 1: FIFO readers take unconditional tickets      */
   int32_t bucket_window;            /* bucket L2: winners >= this many buckets above the
                                        floor bypass L0/L1 (0 = reference cascade)       */
-  int32_t reserved[4];
+  int32_t read_batch;               /* elements per L1 read (0 = lanes_per_group, the
+                                       reference's `want`); up to max(block_size, 32)   */
+  int32_t reserved[3];
 } mlmq_config_t;
 
 /*

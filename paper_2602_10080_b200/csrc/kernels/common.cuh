@@ -63,7 +63,7 @@ enum {
 // Debug-only phase profile slots (per warp, clock64 cycles / counts), MLMQ_DEBUG=1.
 enum {
   P_L0L1 = 0, P_HUB, P_L2R, P_RELAX, P_L2W, P_IDLE, P_NBATCH, P_BATCHSUM, P_NL2R, P_NL2W,
-  P_SPINS, P_CASFAIL, P_L2WELEMS, P_TOTAL, P_COUNT
+  P_SPINS, P_CASFAIL, P_L2WELEMS, P_TOTAL, P_HEAD, P_STEPS, P_COUNT
 };
 constexpr int kMetSlots = 32;  // M_COUNT metric slots + P_COUNT profile slots (smem, per warp)
 constexpr int kProfBase = 16;
@@ -194,6 +194,9 @@ __device__ __forceinline__ void ld_relaxed_v2(const unsigned long long* p, unsig
                                               unsigned long long& b) {
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* a) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
 // atomic min without a return value (RED.MIN at L2)
 __device__ __forceinline__ void red_min(uint32_t* a, uint32_t v) {
   asm volatile("red.relaxed.gpu.global.min.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
@@ -293,6 +296,7 @@ struct KParams {
   int batch_cap, out_cap, spill_cap;  // elements
   int far_cap;                  // far staging elements (bucket window), 0 when unused
   int l1_want;                  // elements per L1 read (reference: lanes_per_group)
+  int adj_prefetch;             // prefetch adjacency list heads into L2 at batch start
   long long ring_margin;        // bucket rings: pending blocks kept free for racing writers
 
   // 1D-partitioned shard; nparts == 1 for an unpartitioned graph

@@ -40,6 +40,7 @@ struct Worker {
   uint32_t* bhist;            // elements per bucket
   uint32_t* bcur;             // scatter cursor per bucket
   uint32_t* bremap;           // bucket -> ring actually written (occupancy-aware)
+  uint32_t* bremap_row;       // expansion: start position -> owner lane (32 entries)
   int lane, gid, L;
 
   // L0: per-lane register FIFO (shift register, pop at index 0)
@@ -80,6 +81,7 @@ struct Worker {
     bhist = reinterpret_cast<uint32_t*>(btick + (p.bscratch ? p.bmax : 0));
     bcur = bhist + (p.bscratch ? p.bmax : 0);
     bremap = bcur + (p.bscratch ? p.bmax : 0);
+    bremap_row = bremap + (p.bscratch ? p.bmax : 0);  // 32 u32: row owner map (expansion)
     l0n = 0;
     wc = rc = l0size = 0;
     h1 = n1 = h2 = n2 = 0;
@@ -300,7 +302,6 @@ struct Worker {
       __nanosleep(ns);
       if (ns < 1024) ns <<= 1;
     }
-    if (kDebug && p.prof) atomicAdd(met + kProfBase + P_SPINS, (unsigned long long)spins);
     return true;
   }
 
@@ -1613,6 +1614,7 @@ struct Worker {
       return;
     }
     for (int base = 0; base < nb; base += 32) {
+      unsigned long long th0 = pclk();
       LOC();
       const int i = base + lane;
       bool valid = i < nb;
@@ -1638,7 +1640,16 @@ struct Worker {
         du = e.d < cur ? e.d : cur;
       }
       if (!valid) lo = hi = 0;
+      // warm L2 with the head of each adjacency list while the warp does the scan and
+      // the first step's address math (the step's loads then hit L2 instead of DRAM)
+      if (valid && p.adj_prefetch) {
+        const uint2* a0 = p.adj + lo;
+        prefetch_l2(a0);
+        if (hi - lo > 16) prefetch_l2(a0 + 16);
+        if (hi - lo > 32) prefetch_l2(a0 + 32);
+      }
       const unsigned vm = __ballot_sync(FULL, valid);
+      pacc(P_HEAD, th0);
       count(M_SETTLED, (unsigned long long)__popc(vm));
       // hub tier: split huge lists into shared edge-range items
       unsigned hm = __ballot_sync(FULL, valid && (hi - lo) > p.hub_thresh);
@@ -1662,32 +1673,39 @@ struct Worker {
       const int incl = warp_incl_scan(ds, lane);
       const int total = __shfl_sync(FULL, incl, 31);
       const int excl = incl - ds;
+      const unsigned long long base_e = lo - (unsigned long long)excl;  // edge = base[owner] + slot
       for (int e0 = 0; e0 < total; e0 += 32 * U) {
         LOC();
+        const unsigned long long tq0 = pclk();
         bool act[U];
         unsigned long long kk[U];
         S dus[U];
 #pragma unroll
         for (int j = 0; j < U; ++j) {
           LOC();
+          // all U rows unconditionally: the 8 independent 5-step shuffle searches
+          // interleave (a per-row branch would serialise them)
           const int idx = e0 + j * 32 + lane;
           int o = 0;
 #pragma unroll
           for (int s = 16; s >= 1; s >>= 1) {
-            LOC();
             const int probe = __shfl_sync(FULL, incl, o + s - 1);
             if (probe <= idx) o += s;
           }
-          const unsigned long long olo = __shfl_sync(FULL, lo, o);
-          const int oex = __shfl_sync(FULL, excl, o);
+          const unsigned long long ob = __shfl_sync(FULL, base_e, o);
           dus[j] = __shfl_sync(FULL, du, o);
           act[j] = idx < total;
-          kk[j] = olo + (unsigned long long)(idx - oex);
+          kk[j] = ob + (unsigned long long)idx;
         }
+        pacc(P_SPINS, tq0);
+        const unsigned long long ts0 = pclk();
         relax_slots(act, kk, dus);
+        pacc(P_STEPS, ts0);
       }
     }
+    const unsigned long long tf0 = pclk();
     flush_out(true);
+    pacc(P_CASFAIL, tf0);
   }
 
   // ============================================================ eager sharing

@@ -275,7 +275,7 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
   s->bscratch = (s->l2k == L2K_BUCKET && c->bmax <= 256) ? 1 : 0;
   s->far_cap = (s->l2k == L2K_BUCKET && c->bucket_window > 0 && c->bmax >= 3) ? kOutCap : 0;
   long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n + s->far_cap) + kMetSlots * 8 +
-                    (s->bscratch ? 20LL * c->bmax : 0LL);
+                    (s->bscratch ? 20LL * c->bmax : 0LL) + 32LL * 4;
   bytes = (bytes + 15) / 16 * 16;
   int max_smem_block = 0;
   CK(cudaDeviceGetAttribute(&max_smem_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
@@ -423,11 +423,12 @@ void debug_dump(mlmq_graph* g, int G, const char* tag) {
   fprintf(stderr,
           "[mlmq debug] %s G=%d cycles/warp=%.3g  L0L1 %.1f%%  hub %.1f%%  L2read %.1f%%  relax %.1f%% "
           "(of which L2write %.1f%%)  idle %.1f%% | batches %llu avg %.1f  L2 reads %llu  L2 writes %llu "
-          "(%.1f elems avg)  spins %llu  casfail %llu\n",
+          "(%.1f elems avg)  search %.1f%%  endflush %.1f%% | relax: head %.1f%% steps %.1f%%\n",
           tag, G, T / G, 100 * tot[P_L0L1] / T, 100 * tot[P_HUB] / T, 100 * tot[P_L2R] / T,
           100 * tot[P_RELAX] / T, 100 * tot[P_L2W] / T, 100 * tot[P_IDLE] / T, tot[P_NBATCH],
           tot[P_NBATCH] ? (double)tot[P_BATCHSUM] / tot[P_NBATCH] : 0.0, tot[P_NL2R], tot[P_NL2W],
-          tot[P_NL2W] ? (double)tot[P_L2WELEMS] / tot[P_NL2W] : 0.0, tot[P_SPINS], tot[P_CASFAIL]);
+          tot[P_NL2W] ? (double)tot[P_L2WELEMS] / tot[P_NL2W] : 0.0, 100 * tot[P_SPINS] / T, 100 * tot[P_CASFAIL] / T,
+          100 * tot[P_HEAD] / T, 100 * tot[P_STEPS] / T);
   int hist[8] = {0};
   int shown = 0;
   for (int i = 0; i < G; ++i) {
@@ -597,10 +598,8 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.out_cap = kOutCap;
   p.spill_cap = sh.spill_cap;
   p.far_cap = sh.far_cap;
-  {
-    const char* w = getenv("MLMQ_L1_WANT");  // experiment knob
-    p.l1_want = std::max(1, std::min(w ? atoi(w) : c->lanes_per_group, sh.batch_cap));
-  }
+  p.l1_want = std::max(1, std::min(c->read_batch > 0 ? c->read_batch : c->lanes_per_group, sh.batch_cap));
+  p.adj_prefetch = 1;
   p.ring_margin = std::min<long long>((long long)w.bn / 2, 4LL * G + 64);
   p.share = c->share ? 1 : 0;
   p.fifo_park = (sh.l2k == L2K_FIFO && c->fifo_park) ? 1 : 0;

@@ -48,6 +48,7 @@ class EngineConfig:
     share: bool = True       # eager write-back to L2 while groups idle (B200 extension)
     fifo_park: bool = True   # FIFO readers park on unconditional tickets
     bucket_window: int = 1   # bucket L2: winners >= this many buckets above the floor skip L0/L1
+    read_batch: int = 64     # elements per L1 read (0 = lanes_per_group, the reference's want)
 
 
 class SsspResult:
@@ -181,6 +182,7 @@ def _native_config(cfg: MlmqConfig, eng: EngineConfig, unit_weights: bool,
     c.share = 1 if eng.share else 0
     c.fifo_park = 1 if eng.fifo_park else 0
     c.bucket_window = max(0, int(eng.bucket_window))
+    c.read_batch = max(0, int(eng.read_batch))
     return c
 
 

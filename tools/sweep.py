@@ -31,6 +31,8 @@ for vals in itertools.product(*[grid[k] for k in keys]):
         cfg2, eng2, dg, ncfg = prepare(g, 0, cfg, eng, features=f)
         ms = []
         for _ in range(int(o.get("reps", 3))):
+            if o.get("unit", "0") == "1":
+                ncfg.unit_weights = 1
             m = dg.sssp_device(0, ncfg)
             ms.append(m.kernel_ms)
         if e_reach is None:
