@@ -9,7 +9,7 @@ n = int(sys.argv[6]) if len(sys.argv) > 6 else 2
 g = build_graph(name)
 f = extract_features(g)
 aw = max(1, round(f.avg_weight))
-cfg = MlmqConfig(l1_type=l1, l2_type=l2, l0_capacity=1, l1_params=L1Params(capacity=cap, filter_f=4 * aw),
+cfg = MlmqConfig(l1_type=l1, l2_type=l2, l0_capacity=int(os.environ.get('L0', '4')), l1_params=L1Params(capacity=cap, filter_f=4 * aw),
                  l2_params=L2Params(delta=int(ds * aw) if l2 == "bucket" else None), num_groups=None)
 cfg, eng, dg, ncfg = prepare(g, 0, cfg, EngineConfig(), features=f)
 for _ in range(n):
