@@ -132,13 +132,15 @@ __global__ void audit_kernel(KParams p, unsigned long long* out, int fifo_fix) {
     for (int i = 0; i < 4; ++i) out[8 + i] = ctl[C_DIAG + i];
     out[12] = ctl[C_HUB_ITEMS];
     out[13] = ctl[C_EPOCH];
-    if (fifo_fix) {
-      const unsigned long long w = p.ptrs[0], rd = p.ptrs[16];
-      for (unsigned long long tk = w; tk < rd; ++tk) p.seq[tk & p.bn_mask] = tk + p.bn_mask + 1;
-      if (rd > w) p.ptrs[0] = rd;
-      __threadfence();
-    }
     if (kDebug && p.wstate) p.wstate[2 * (size_t)p.G + 5] = 2;
+  }
+  if (fifo_fix) {  // retire the parked FIFO tickets, all threads in parallel
+    __syncthreads();
+    const unsigned long long w = p.ptrs[0], rd = p.ptrs[16];
+    for (unsigned long long tk = w + t; tk < rd; tk += blockDim.x) p.seq[tk & p.bn_mask] = tk + p.bn_mask + 1;
+    __syncthreads();
+    if (t == 0 && rd > w) p.ptrs[0] = rd;
+    __threadfence();
   }
 }
 
