@@ -360,3 +360,17 @@ def test_sharded_equals_unsharded_on_c2():
     for P in (2, 8):
         res = sssp_solve_sharded(g, 0, P, MlmqConfig(l2_type="fifo"))
         assert np.array_equal(res.local_dist, want), P
+
+
+def test_recycled_result_buffers_are_not_aliased():
+    # results live in page-locked buffers recycled across solves: a held result must
+    # never be overwritten by a later solve
+    g = generate_graph("rmat", seed=4, scale=12, edge_factor=8, wmin=1, wmax=99)
+    r0 = sssp_solve(g, 0)
+    r1 = sssp_solve(g, 17)
+    r2 = sssp_solve(g, 99)
+    del r1
+    r3 = sssp_solve(g, 5)
+    assert np.array_equal(r0.dist_array, oracle_dist(g, 0))
+    assert np.array_equal(r2.dist_array, oracle_dist(g, 99))
+    assert np.array_equal(r3.dist_array, oracle_dist(g, 5))
