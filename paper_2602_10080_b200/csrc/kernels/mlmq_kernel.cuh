@@ -25,7 +25,10 @@ struct Worker {
   using Tr = DT<K>;
   using S = typename Tr::S;
   using E = Elem<S>;
-  static constexpr int U = 8;  // edge slots per lane per step (8 independent loads in flight)
+#ifndef MLMQ_U
+#define MLMQ_U 4  // measured on B200 (C2): U=2 2.26 ms, 3 1.69, 4 1.64, 5 1.78, 6 1.88, 8 1.98, 12 2.82
+#endif
+  static constexpr int U = MLMQ_U;  // edge slots per lane per step (U independent loads in flight)
 
   const KParams& p;
   S* dist;

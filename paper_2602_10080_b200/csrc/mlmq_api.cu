@@ -124,7 +124,7 @@ using namespace mlmq;
 namespace {
 
 constexpr int kWarpsPerBlockMax = 9;  // 2 CTAs x 9 warps fit the 111-register K1
-constexpr int kOutCap = 32 * 8 + 32;  // L - 1 carried + 32 lanes x U=8 winners
+constexpr int kOutCap = 32 * 8 + 32;  // L - 1 carried + 32 lanes x U (<= 8) winners
 constexpr int kAuditWords = 14;
 
 struct Workspace {
