@@ -1535,23 +1535,41 @@ struct Worker {
     int got = 0;
     unsigned long long tk = 0, c = 0;
     HubItem it = HubItem();
+    // The window of 8 descriptors from the head is inspected by 8 lanes at once (one
+    // round trip instead of up to 24 dependent ones when many hub lists are live).
+    unsigned long long h = 0, w = 0;
     if (lane == 0) {
-      unsigned long long h = ld_relaxed(p.ctl + C_HUB_RP);
-      const unsigned long long w = ld_relaxed(p.ctl + C_HUB_WP);
-      const unsigned long long h0 = h;
-      for (unsigned long long d = h; d < w && d < h0 + 8 && !got; ++d) {
-        const unsigned long long slot = d & p.hub_mask;
-        const unsigned long long s = ld_acquire(p.hub_seq + slot);
-        if (s != d + 1) {
-          if (s > d + 1 && d == h) h = d + 1;  // freed: the head may move past it
-          continue;                            // not yet published
-        }
-        const unsigned long long x0 = ld_relaxed(p.hub_next + slot);
-        const uint32_t nch0 = __ldcg(&p.hub_data[slot].pad);
-        if ((x0 >> kClaimBits) == d && (x0 & kClaimMask) >= nch0) {
-          if (d == h) h = d + 1;  // exhausted
-          continue;
-        }
+      h = ld_relaxed(p.ctl + C_HUB_RP);
+      w = ld_relaxed(p.ctl + C_HUB_WP);
+    }
+    h = __shfl_sync(FULL, h, 0);
+    w = __shfl_sync(FULL, w, 0);
+    if (h >= w) return false;
+    bool cand = false, finished = false;
+    if (lane < 8 && h + lane < w) {
+      const unsigned long long d = h + lane, slot = d & p.hub_mask;
+      const unsigned long long s = ld_acquire(p.hub_seq + slot);
+      const unsigned long long x0 = ld_relaxed(p.hub_next + slot);
+      const uint32_t nch0 = __ldcg(&p.hub_data[slot].pad);
+      if (s > d + 1) {
+        finished = true;  // freed
+      } else if (s == d + 1) {
+        const bool exhausted = (x0 >> kClaimBits) == d && (x0 & kClaimMask) >= nch0;
+        finished = exhausted;
+        cand = !exhausted;
+      }
+    }
+    const unsigned cm = __ballot_sync(FULL, cand);
+    const unsigned fm = __ballot_sync(FULL, finished);
+    const int adv = __ffs(~fm) - 1;  // leading run of finished descriptors from the head
+    if (lane == 0 && adv > 0) atomicCAS(p.ctl + C_HUB_RP, h, h + (unsigned long long)adv);  // best effort
+    if (cm == 0) return false;
+    if (lane == 0) {
+      unsigned rem = cm;
+      while (rem && !got) {
+        const int l = __ffs(rem) - 1;
+        rem &= rem - 1;
+        const unsigned long long d = h + (unsigned long long)l, slot = d & p.hub_mask;
         const unsigned long long x = atomicAdd(p.hub_next + slot, 1ull);
         tk = x >> kClaimBits;
         c = x & kClaimMask;
@@ -1574,9 +1592,7 @@ struct Worker {
           if (stopped()) break;
           __nanosleep(32);
         }
-        if (!got && tk == d && d == h) h = d + 1;
       }
-      if (h != h0) atomicCAS(p.ctl + C_HUB_RP, h0, h);  // best effort
     }
     if (!__shfl_sync(FULL, got, 0)) return false;
     tk = __shfl_sync(FULL, tk, 0);
