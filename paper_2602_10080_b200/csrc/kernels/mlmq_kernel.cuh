@@ -1967,7 +1967,10 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
 }
 
 template <int K, int L2K, int CM, int L1T>
-__global__ void __launch_bounds__(288, 2) mlmq_persistent_kernel(const __grid_constant__ KParams p) {
+#ifndef MLMQ_MINB
+#define MLMQ_MINB 2
+#endif
+__global__ void __launch_bounds__(288, MLMQ_MINB) mlmq_persistent_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = blockIdx.x * (blockDim.x >> 5) + warp;

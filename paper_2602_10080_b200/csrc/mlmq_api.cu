@@ -123,7 +123,7 @@ using namespace mlmq;
 
 namespace {
 
-constexpr int kWarpsPerBlockMax = 9;  // 2 CTAs x 9 warps fit the 111-register K1
+constexpr int kWarpsPerBlockMax = 9;  // 9 warps per CTA (launch bounds 288 threads)
 constexpr int kOutCap = 32 * 8 + 32;  // L - 1 carried + 32 lanes x U (<= 8) winners
 constexpr int kAuditWords = 14;
 
