@@ -93,8 +93,6 @@ def lib():
         path = LIB_PATH
         if os.environ.get("MLMQ_DEBUG") == "1" and os.path.exists(DEBUG_LIB_PATH):
             path = DEBUG_LIB_PATH
-        if os.environ.get("MLMQ_LIB"):  # experiment builds (another in-tree libmlmq variant)
-            path = os.path.join(_HERE, os.environ["MLMQ_LIB"])
         if not os.path.exists(path):
             raise EngineError(
                 f"{path} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`"

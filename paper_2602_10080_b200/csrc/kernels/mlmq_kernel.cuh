@@ -1937,7 +1937,9 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
       far = warp_sum_u64(far);
       first = __reduce_min_sync(FULL, first);
       kq = (far > 0 && d == r - far) ? kq + 1 : 0;
-      if (kq >= 2 && first < p.bmax) {
+      // one observation suffices: the counters are monotone and done was read first, and
+      // an early advance would only cost work efficiency, never correctness
+      if (kq >= 1 && first < p.bmax) {
         if (lane == 0) {
           st_release(p.ctl + C_EPOCH, e + (unsigned long long)first);
           red_add(p.ctl + C_GEN, 1ull);
@@ -1962,7 +1964,7 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
       if (lane == 0) st_release(p.ctl + C_STOP, 1ull);
       break;
     }
-    __nanosleep(256);
+    __nanosleep(p.bwin > 0 ? 64 : 256);  // a managed floor is latency-critical
   }
 }
 

@@ -26,7 +26,8 @@ for vals in itertools.product(*[grid[k] for k in keys]):
                      num_groups=None if o.get("groups", "auto") == "auto" else int(o["groups"]),
                      lanes_per_group=int(o.get("lanes", 32)))
     eng = EngineConfig(hub_chunk=int(o.get("hub", 0)), share=o.get("share", "1") == "1",
-                       fifo_park=o.get("park", "1") == "1", bucket_window=int(o.get("win", 1)))
+                       fifo_park=o.get("park", "1") == "1", bucket_window=int(o.get("win", 1)),
+                       read_batch=int(o.get("rb", 64)))
     try:
         cfg2, eng2, dg, ncfg = prepare(g, 0, cfg, eng, features=f)
         ms = []
