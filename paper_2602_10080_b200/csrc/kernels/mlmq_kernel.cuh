@@ -1843,7 +1843,10 @@ struct Worker {
         backoff = 0;
         continue;
       }
-      if (L2K == L2K_BUCKET && nfar > 0) far_flush();  // staged far work leaves before idling
+      if (L2K == L2K_BUCKET && nfar > 0) {  // staged far work leaves before idling, and the
+        far_flush();                        // cascade runs once more: with bnum > 1 some of
+        continue;                           // it may be readable by this very group
+      }
       if (!idle) {
         idle = true;
         seen = ~0ull;  // the first miss re-checks once against a generation read before it
