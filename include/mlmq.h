@@ -79,14 +79,16 @@ typedef struct {
   int32_t dist_mode;                /* MLMQ_DIST_*                                    */
   double watchdog_s;                /* engine.py:267-279; <= 0 disables               */
   double spin_timeout_s;            /* ring-slot wait before QueueOverflowError (l2.py:94) */
-  int32_t hub_chunk;                /* edges per hub work item (0 = library default)  */
+  int32_t hub_chunk;                /* edges per hub chunk (0 = library default 2048) */
   int32_t share;                    /* 1: eager L1/L0 write-back while groups are idle */
   int32_t fifo_park;                /* 1: FIFO readers take unconditional tickets      */
   int32_t bucket_window;            /* bucket L2: winners >= this many buckets above the
                                        floor bypass L0/L1 (0 = reference cascade)       */
   int32_t read_batch;               /* elements per L1 read (0 = lanes_per_group, the
                                        reference's `want`); up to max(block_size, 32)   */
-  int32_t reserved[3];
+  int32_t hub_threshold;            /* lists longer than this become hub descriptors
+                                       (0 = 4 x hub_chunk)                              */
+  int32_t reserved[2];
 } mlmq_config_t;
 
 /*

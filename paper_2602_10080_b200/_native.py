@@ -45,7 +45,7 @@ class Config(ctypes.Structure):
         ("watchdog_s", ctypes.c_double), ("spin_timeout_s", ctypes.c_double),
         ("hub_chunk", ctypes.c_int32), ("share", ctypes.c_int32), ("fifo_park", ctypes.c_int32),
         ("bucket_window", ctypes.c_int32), ("read_batch", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 3),
+        ("hub_threshold", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
     ]
 
 

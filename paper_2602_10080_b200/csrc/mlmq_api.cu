@@ -507,7 +507,7 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     set_last_error("num_groups=%d exceeds the %d groups the device keeps resident for this configuration", G, sh.max_groups);
     return MLMQ_EINVAL;
   }
-  const unsigned long long hub_chunk = c->hub_chunk > 0 ? std::min<unsigned long long>((unsigned long long)c->hub_chunk, 1ull << 20) : 3072ull;
+  const unsigned long long hub_chunk = c->hub_chunk > 0 ? std::min<unsigned long long>((unsigned long long)c->hub_chunk, 1ull << 20) : 2048ull;
   if ((st = ensure_workspace(g, c, sh, hub_chunk, G))) return st;
   if (g->metrics_cap < (unsigned long long)G) {
     cudaFree(g->d_metrics);
@@ -585,7 +585,13 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.hub_fin = w.hub_fin;
   p.hub_mask = w.hub_cap - 1;
   p.hub_chunk = hub_chunk;
-  p.hub_thresh = 2 * hub_chunk;
+  // lists above the threshold become hub descriptors; measured on C2 (chunk 2048):
+  // threshold 4096 2.93 ms, 6144 1.53, 8192 1.51, 12288 1.55, 16384 1.63
+  // (clamped so a warp's flattened expansion of 32 lists stays within int range)
+  p.hub_thresh = c->hub_threshold > 0
+                     ? std::min<unsigned long long>(std::max<unsigned long long>((unsigned long long)c->hub_threshold, hub_chunk),
+                                                    1ull << 24)
+                     : 4 * hub_chunk;
   p.ctl = g->d_ctl;
   p.host_abort = g->d_abort;
   p.metrics = g->d_metrics;

@@ -49,6 +49,7 @@ class EngineConfig:
     fifo_park: bool = True   # FIFO readers park on unconditional tickets
     bucket_window: int = 1   # bucket L2: winners >= this many buckets above the floor skip L0/L1
     read_batch: int = 64     # elements per L1 read (0 = lanes_per_group, the reference's want)
+    hub_threshold: int = 0   # lists longer than this become hub descriptors (0 = 4 x hub_chunk)
 
 
 class SsspResult:
@@ -183,6 +184,7 @@ def _native_config(cfg: MlmqConfig, eng: EngineConfig, unit_weights: bool,
     c.fifo_park = 1 if eng.fifo_park else 0
     c.bucket_window = max(0, int(eng.bucket_window))
     c.read_batch = max(0, int(eng.read_batch))
+    c.hub_threshold = max(0, int(eng.hub_threshold))
     return c
 
 
