@@ -311,15 +311,20 @@ int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& s
     need.nrings = 0;
     need.bn = 1;
     need.nheaps = c->l2_type == MLMQ_L2_MULTI ? c->pnum : 1;
-    unsigned long long total = std::max<unsigned long long>(65536ull, 4ull * n + 4096ull);
-    need.hcap = std::max<unsigned long long>(256ull, total / (unsigned long long)need.nheaps);
+    // nodes hold <= node_batch elements: small batches need proportionally more nodes;
+    // writers rotate over the heaps, so each heap gets twice its even share
+    const unsigned long long nb = (unsigned long long)std::max(1, std::min(c->node_batch, 32));
+    const unsigned long long total =
+        std::max<unsigned long long>(65536ull, (4ull * n + 4096ull) * std::min<unsigned long long>(8ull, (32ull + nb - 1) / nb));
+    need.hcap = std::max<unsigned long long>(1024ull, 2ull * total / (unsigned long long)need.nheaps);
   } else {
     need.nrings = sh.l2k == L2K_BUCKET ? c->bmax : 1;
     const unsigned long long slots = 8ull * n / (unsigned long long)c->block_size + 16384ull;
-    // bucket rings: a quarter of the FIFO ring each, and room for every group to race
-    // a few blocks into a ring past the occupancy check (ring_margin)
+    // bucket rings: a quarter of the FIFO ring each (the whole of it with one bucket), and
+    // room for every group to race a few blocks into a ring past the occupancy check
     unsigned long long per = sh.l2k == L2K_BUCKET
-                                 ? std::max<unsigned long long>(slots / 4 + 1024, 16ull * (unsigned long long)groups + 1024ull)
+                                 ? std::max<unsigned long long>(slots / (unsigned long long)std::min(4, std::max(1, c->bmax)) + 1024,
+                                                                16ull * (unsigned long long)groups + 1024ull)
                                  : slots;
     need.bn = next_pow2(std::max<unsigned long long>((unsigned long long)c->block_num, per));
     need.nheaps = 0;
