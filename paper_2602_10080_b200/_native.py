@@ -21,6 +21,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmlmq.so")
 #: MLMQ_DEBUG=1 loads the debug build (make -C csrc debug): phase profile + wait states
 DEBUG_LIB_PATH = os.path.join(_HERE, "libmlmq_debug.so")
+#: MLMQ_DEBUG=1 MLMQ_PROFILE=1 loads the profile build (make -C csrc prof): the same hooks
+#: without the per-line trace, so the phase split is representative
+PROF_LIB_PATH = os.path.join(_HERE, "libmlmq_prof.so")
 
 MLMQ_OK, MLMQ_EINVAL, MLMQ_EOVERFLOW, MLMQ_EENGINE, MLMQ_ECUDA, MLMQ_ENOMEM = range(6)
 W_U32, W_F32, W_UNIT = 0, 1, 2
@@ -90,9 +93,11 @@ def lib():
     with _lib_lock:
         if _lib is not None:
             return _lib
-        path = LIB_PATH
-        if os.environ.get("MLMQ_DEBUG") == "1" and os.path.exists(DEBUG_LIB_PATH):
-            path = DEBUG_LIB_PATH
+        path = os.environ.get("MLMQ_LIB") or LIB_PATH  # experiment builds (make KSET=...)
+        if os.environ.get("MLMQ_DEBUG") == "1" and not os.environ.get("MLMQ_LIB"):
+            want = PROF_LIB_PATH if os.environ.get("MLMQ_PROFILE") == "1" else DEBUG_LIB_PATH
+            if os.path.exists(want):
+                path = want
         if not os.path.exists(path):
             raise EngineError(
                 f"{path} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`"
@@ -204,6 +209,15 @@ def pinned_empty(n: int, dtype) -> np.ndarray:
     return np.frombuffer(buf, dtype=dt, count=int(n))
 
 
+def _note_no_device():
+    """Test hook: tests/test_reference_suite.py runs the reference suites on a GPU-less host
+    and needs to know which tests stopped at the missing device (MLMQ_NODEV_LOG)."""
+    log = os.environ.get("MLMQ_NODEV_LOG")
+    if log:
+        with open(log, "a") as fh:
+            fh.write((os.environ.get("PYTEST_CURRENT_TEST") or "?").split(" ")[0] + "\n")
+
+
 def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data
 
@@ -215,6 +229,7 @@ class DeviceGraph:
                  weight_kind: int, device: int = 0):
         L = lib()
         if device_count() < 1:
+            _note_no_device()
             raise EngineError("no CUDA device is visible; the MLMQ engine has no CPU fallback")
         self._lib = L
         self.row_offsets = np.ascontiguousarray(row_offsets, dtype=np.uint64)
@@ -299,6 +314,7 @@ class DeviceShard(DeviceGraph):
                  weight_kind: int, n_global: int, rank: int, nparts: int, device: int = 0):
         L = lib()
         if device_count() < 1:
+            _note_no_device()
             raise EngineError("no CUDA device is visible; the MLMQ engine has no CPU fallback")
         self._lib = L
         self.row_offsets = np.ascontiguousarray(row_offsets, dtype=np.uint64)

@@ -8,9 +8,10 @@ the rule list (cli.py:248-260).  Distances are inlined (``null`` = unreachable) 
 ``--max-inline-distances`` vertices, otherwise written to a ``.distances.u64`` sidecar
 (little-endian u64, all-ones = unreachable, engine.py:385-387).
 
-B200 differences: ``--num-groups`` defaults to ``auto`` (every warp the device keeps
-resident; ``$MLQ_NUM_GROUPS`` or an integer overrides it), ``--device`` picks the GPU, and
-``solve`` reports the device time next to the reference's metrics.
+B200 differences: ``--num-groups`` keeps the reference default ($MLQ_NUM_GROUPS or 4, one
+warp per group) and also takes ``auto`` (every warp the device keeps resident, resolved to
+an integer before any config is emitted, so the schemas stay valid); ``--device`` picks the
+GPU; ``solve`` reports the device time next to the reference's metrics.
 
     python -m paper_2602_10080_b200.cli solve --gen rmat:16,16,1,255 --source 0
     python -m mlq_sssp.cli verify --gen grid2d:64x64,1,100 --l1 filter --l2 bucket
@@ -110,9 +111,30 @@ def _load(args) -> Tuple[CsrGraph, dict]:
     return g, origin
 
 
-def _groups(args) -> Optional[int]:
-    v = args.num_groups if args.num_groups is not None else os.environ.get(ENV_NUM_GROUPS, "auto")
-    return None if str(v) == "auto" else int(v)
+def _num_groups_arg(text: str):
+    """--num-groups: a positive integer, or ``auto`` (every warp the device keeps resident)."""
+    if str(text).strip().lower() == "auto":
+        return "auto"
+    return int(text)
+
+
+def _groups(args, default=None):
+    """cli.py:195-201: explicit flag, else $MLQ_NUM_GROUPS, else the reference's 4.
+    ``auto`` becomes None here and is resolved to an integer against the device."""
+    v = args.num_groups
+    if v is None:
+        v = os.environ.get(ENV_NUM_GROUPS) or (4 if default is None else default)
+    return None if str(v).strip().lower() == "auto" else int(v)
+
+
+def _concrete(cfg: MlmqConfig, g: CsrGraph, feats, args) -> MlmqConfig:
+    """Resolve ``auto`` groups to the device's integer so emitted configs stay
+    schema-valid (common.schema.json:63,73 require an integer)."""
+    if cfg.num_groups is not None:
+        return cfg
+    from .engine import prepare
+    resolved, _, _, _ = prepare(g, 0, cfg, EngineConfig(device=getattr(args, "device", 0)), features=feats)
+    return resolved
 
 
 def _explicit(args) -> Optional[MlmqConfig]:
@@ -232,48 +254,78 @@ def cmd_select(args) -> int:
            "selector": "model" if model is not None else "rule_based",
            "ranking": [{"rank": i + 1, "candidate": asdict(c), "score": s, "label": c.label()}
                        for i, (c, s) in enumerate(top)],
-           "bound_config": ranked[0][0].bind(feats, num_groups=_groups(args)).to_json_dict()}
+           "bound_config": _concrete(ranked[0][0].bind(feats, num_groups=_groups(args)), g, feats,
+                                     args).to_json_dict()}
     if model is not None:
         out["model"] = {"path": path, "corpus_hash": model.corpus_hash, "trees": len(model.trees)}
     _emit(out, args.out)
     return EXIT_OK
 
 
+def _csv_list(text, conv=str):
+    return None if text is None else [conv(x.strip()) for x in text.split(",") if x.strip()]
+
+
 def cmd_bench(args) -> int:
-    graphs = []
-    for spec in args.gen_list:
+    """cli.py:457-534: time a candidate grid over --graph/--gen inputs into a records CSV.
+    The GPU engine records the device time of each solve (``timing``)."""
+    graphs = [(path, load_graph(path, fmt=args.format, weight_scale=args.weight_scale))
+              for path in (args.graph or [])]
+    for spec in args.gen or []:
         kind, params = parse_gen_spec(spec)
-        graphs.append((spec, generate_graph(kind, seed=args.gen_seed, **params)))
-    recs = benchmark_graphs(graphs, enumerate_candidates(), reps=args.reps,
-                            num_groups=_groups(args), timing="kernel")
-    write_records_csv(recs, args.records)
-    _emit({"subcommand": "bench", "records": args.records, "graphs": len(graphs),
-           "rows": len(recs), "timing": "kernel"})
+        graphs.append((f"{spec}@{args.gen_seed}", generate_graph(kind, seed=args.gen_seed, **params)))
+    if not graphs:
+        raise ValueError("bench needs at least one --graph or --gen")
+    grid = {k: v for k, v in (("l1", _csv_list(args.grid_l1)), ("l2", _csv_list(args.grid_l2)),
+                              ("delta_scale", _csv_list(args.delta_scales, float)),
+                              ("wb", _csv_list(args.wb_list, int))) if v}
+    cands = enumerate_candidates(grid or None)
+    if not cands:
+        raise ValueError("the candidate grid is empty")
+    groups = _groups(args, default=1)
+    recs = benchmark_graphs(graphs, cands, source=args.source, reps=args.reps, num_groups=groups,
+                            watchdog_s=args.watchdog, timing=args.timing)
+    write_records_csv(recs, args.out)
+    best = {}
+    for r in recs:
+        if r.graph_id not in best or r.wall_time_us < best[r.graph_id]["wall_time_us"]:
+            best[r.graph_id] = {"label": r.label(), "wall_time_us": r.wall_time_us}
+    # figures need matplotlib (absent in this image); the record CSV carries the data
+    _emit({"subcommand": "bench", "records": args.out, "rows": len(recs), "graphs": len(graphs),
+           "candidates": len(cands), "reps": args.reps, "source": args.source,
+           "num_groups": groups if groups is not None else
+           _concrete(cands[0].bind(extract_features(graphs[0][1]), num_groups=None), graphs[0][1],
+                     extract_features(graphs[0][1]), args).num_groups,
+           "figures": [], "best_per_graph": best, "timing": args.timing})
     return EXIT_OK
 
 
 def cmd_train(args) -> int:
     recs = read_records_csv(args.records)
-    model = train_selector(recs, seed=args.seed, n_trees=args.trees, max_depth=args.max_depth,
+    model = train_selector(recs, seed=args.seed, n_trees=args.trees, max_depth=args.depth,
                            min_leaf=args.min_leaf)
-    model.save(args.model_out)
-    _emit({"subcommand": "train", "records": args.records, "model": args.model_out,
-           "corpus_hash": model.corpus_hash, "trees": len(model.trees)})
+    model.save(args.out)
+    _emit({"subcommand": "train", "records": args.records, "rows": len(recs),
+           "graphs": len({r.graph_id for r in recs}),
+           "configs": len({tuple(r.encoding) for r in recs}), "model": args.out,
+           "trees": len(model.trees), "seed": args.seed, "corpus_hash": model.corpus_hash})
     return EXIT_OK
 
 
 def build_parser() -> argparse.ArgumentParser:
+    """The reference's subcommands and flags (cli.py:541-611), plus ``--device`` and
+    ``--num-groups auto``."""
     ap = argparse.ArgumentParser(prog="mlq", description="MLMQ SSSP on B200 (reference-compatible CLI)")
-    ap.add_argument("--version", action="version", version=__version__)
-    sub = ap.add_subparsers(dest="cmd", required=True)
+    ap.add_argument("--version", action="version", version=f"%(prog)s {__version__}")
+    sub = ap.add_subparsers(dest="subcommand", required=True)
 
     def inputs(p):
-        p.add_argument("--graph")
+        p.add_argument("--graph", help="graph file (.gr DIMACS or .mtx Matrix Market)")
         p.add_argument("--format", choices=("dimacs", "mm"))
-        p.add_argument("--gen")
+        p.add_argument("--gen", help="generator spec, e.g. path:1000 or grid2d:30x40,1,100")
         p.add_argument("--gen-seed", type=int, default=0)
         p.add_argument("--weight-scale", type=int, default=1000)
-        p.add_argument("--out")
+        p.add_argument("--device", type=int, default=0, help="CUDA device (B200 extension)")
 
     def queue(p):
         p.add_argument("--l1", choices=L1_TYPES)
@@ -281,55 +333,77 @@ def build_parser() -> argparse.ArgumentParser:
         for f in ("wb", "delta", "delta-nf", "filter-f", "l1-capacity", "l0-capacity", "block-size",
                   "block-num", "bmax", "bnum", "node-batch", "pnum"):
             p.add_argument("--" + f, type=int)
-        p.add_argument("--auto", action="store_true")
+        p.add_argument("--auto", action="store_true", help=f"rank the grid with ${ENV_MODEL}'s model")
         p.add_argument("--model")
-        p.add_argument("--num-groups", help="integer or 'auto' (default $MLQ_NUM_GROUPS or auto)")
+        p.add_argument("--num-groups", type=_num_groups_arg,
+                       help=f"worker groups (warps) or 'auto'; default ${ENV_NUM_GROUPS} or 4")
         p.add_argument("--lanes", type=int)
         p.add_argument("--th-v", type=int)
         p.add_argument("--seed", type=int, default=0)
         p.add_argument("--no-dup-elim", action="store_true")
         p.add_argument("--watchdog", type=float, default=60.0)
-        p.add_argument("--device", type=int, default=0)
 
-    p = sub.add_parser("gen")
+    p = sub.add_parser("gen", help="generate a graph file")
     p.add_argument("spec")
     p.add_argument("--gen-seed", type=int, default=0)
-    p.add_argument("--format", choices=("dimacs", "mm"))
     p.add_argument("--out", required=True)
+    p.add_argument("--format", choices=("dimacs", "mm"))
     p.set_defaults(fn=cmd_gen)
-    p = sub.add_parser("features")
+
+    p = sub.add_parser("features", help="print the eight selector features")
     inputs(p)
+    p.add_argument("--out")
     p.set_defaults(fn=cmd_features)
+
     for name, fn in (("solve", cmd_solve), ("verify", cmd_verify)):
         p = sub.add_parser(name)
         inputs(p)
         queue(p)
         p.add_argument("--source", type=int, default=0)
         p.add_argument("--unit-weights", action="store_true")
-        p.add_argument("--max-inline-distances", type=int, default=MAX_INLINE)
+        if name == "solve":
+            p.add_argument("--max-inline-distances", type=int, default=MAX_INLINE)
+        p.add_argument("--out")
         p.set_defaults(fn=fn)
-    p = sub.add_parser("select")
+
+    p = sub.add_parser("select", help="rank queue configs for an input")
     inputs(p)
-    p.add_argument("--auto", action="store_true")
     p.add_argument("--model")
-    p.add_argument("--num-groups")
-    p.add_argument("--top", type=int, default=0)
+    p.add_argument("--auto", action="store_true")
+    p.add_argument("--num-groups", type=_num_groups_arg)
+    p.add_argument("--top", type=int, default=3)
+    p.add_argument("--out")
     p.set_defaults(fn=cmd_select)
-    p = sub.add_parser("bench")
-    p.add_argument("gen_list", nargs="+", metavar="SPEC")
-    p.add_argument("--gen-seed", type=int, default=0)
-    p.add_argument("--reps", type=int, default=3)
-    p.add_argument("--num-groups")
+
+    p = sub.add_parser("train", help="fit the selector on benchmark records")
     p.add_argument("--records", required=True)
-    p.set_defaults(fn=cmd_bench)
-    p = sub.add_parser("train")
-    p.add_argument("--records", required=True)
-    p.add_argument("--model-out", required=True)
-    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--out", required=True, help="model file to write")
     p.add_argument("--trees", type=int, default=64)
-    p.add_argument("--max-depth", type=int, default=6)
+    p.add_argument("--depth", type=int, default=6)
     p.add_argument("--min-leaf", type=int, default=2)
+    p.add_argument("--seed", type=int, default=0)
     p.set_defaults(fn=cmd_train)
+
+    p = sub.add_parser("bench", help="time a config grid over a graph corpus")
+    p.add_argument("--graph", action="append")
+    p.add_argument("--format", choices=("dimacs", "mm"))
+    p.add_argument("--gen", action="append")
+    p.add_argument("--gen-seed", type=int, default=0)
+    p.add_argument("--weight-scale", type=int, default=1000)
+    p.add_argument("--grid-l1")
+    p.add_argument("--grid-l2")
+    p.add_argument("--delta-scales")
+    p.add_argument("--wb-list")
+    p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--source", type=int, default=0)
+    p.add_argument("--num-groups", type=_num_groups_arg, help="worker groups while timing (default 1)")
+    p.add_argument("--watchdog", type=float, default=60.0)
+    p.add_argument("--no-figures", action="store_true")
+    p.add_argument("--timing", choices=("wall", "kernel"), default="wall",
+                   help="record host wall time (reference) or device time (B200 extension)")
+    p.add_argument("--device", type=int, default=0)
+    p.add_argument("--out", required=True, help="records CSV to write")
+    p.set_defaults(fn=cmd_bench)
     return ap
 
 

@@ -407,9 +407,9 @@ struct Worker {
   // exists, then wait for the in-flight writer; never leaves a dangling claim.
   __device__ int ring_read(int rid, E* dst) {
     LOC();
-    unsigned long long r = 0;
+    unsigned long long r = 0, elo = 0;
     int got = 0;
-    bool ok = true;
+    bool ok = true, empty = false;
     if (lane == 0) {
       unsigned long long* rpp = rp(rid);
       unsigned long long* wpp = wp(rid);
@@ -418,17 +418,18 @@ struct Worker {
       if (r < w) {
         // One fetch-add claims a ticket (no CAS retry storm).  A racing reader can
         // over-claim past the write pointer; it then either waits for the writer that
-        // already owns its ticket, or -- when the write pointer stands exactly at its
-        // ticket -- takes the ticket as a writer and publishes an EMPTY block, which it
-        // consumes itself (reserve and done both count it), so no claim is ever left
-        // dangling (the audit's "no pending tickets", engine.py:241-242).
+        // already owns its ticket, or takes every ticket from the write pointer up to
+        // its own as a writer (ONE CAS) and publishes them as EMPTY blocks: each is
+        // consumed by the over-claimer that holds it (reserve and done both count it),
+        // so no claim is ever left dangling (the audit's "no pending tickets",
+        // engine.py:241-242), and a burst of k over-claims resolves in one round trip
+        // instead of a k-long chain of CAS hand-offs.
         r = atomicAdd(rpp, 1ull);
         got = 1;
-        bool empty = false;
         unsigned long long t0 = 0;
         int spins = 0;
         while ((w = ld_relaxed(wpp)) <= r) {
-          if (w == r && atomicCAS(wpp, r, r + 1) == r) { empty = true; break; }
+          if (atomicCAS(wpp, w, r + 1) == w) { empty = true; elo = w; break; }
           if (++spins % 64 == 0) {
             if (stopped()) { ok = false; break; }
             const unsigned long long now = globaltimer_ns();
@@ -441,25 +442,31 @@ struct Worker {
           }
           __nanosleep(32);
         }
-        const unsigned long long slot = r & p.bn_mask;
-        if (ok && empty) {
-          ok = lane_spin(seq_ptr(rid, slot), r, rid, slot);  // slot free for ticket r
-          if (ok) {
-            p.cnt[(size_t)rid * (p.bn_mask + 1) + slot] = 0u;
-            st_release(seq_ptr(rid, slot), r + 1);
-          }
-        }
-        if (ok) {
-          wstate(W_RING_READ, r + 1);
-          ok = lane_spin(seq_ptr(rid, slot), r + 1, rid, slot);
-          wstate(W_NONE, 0);
-        }
       }
     }
     got = __shfl_sync(FULL, got, 0);
     if (!got) return 0;
     r = __shfl_sync(FULL, r, 0);
     count(M_L2A, 1);
+    if (__shfl_sync(FULL, (int)empty, 0)) {  // publish the empty blocks elo..r, lanes in parallel
+      elo = __shfl_sync(FULL, elo, 0);
+      for (unsigned long long t = elo + (unsigned long long)lane; t <= r; t += 32) {
+        const unsigned long long slot = t & p.bn_mask;
+        if (ok && lane_spin(seq_ptr(rid, slot), t, rid, slot)) {  // slot free for ticket t
+          p.cnt[(size_t)rid * (p.bn_mask + 1) + slot] = 0u;
+          st_release(seq_ptr(rid, slot), t + 1);
+        } else {
+          ok = false;
+        }
+      }
+      ok = __all_sync(FULL, ok);
+    }
+    if (lane == 0 && ok) {
+      const unsigned long long slot = r & p.bn_mask;
+      wstate(W_RING_READ, r + 1);
+      ok = lane_spin(seq_ptr(rid, slot), r + 1, rid, slot);
+      wstate(W_NONE, 0);
+    }
     if (!__shfl_sync(FULL, (int)ok, 0)) return 0;
     __syncwarp();
     return take_block(rid, r, dst);

@@ -267,6 +267,10 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
   s->l2k = l2_kind(c->l2_type);
   s->cm = c->l0_capacity <= 4 ? 4 : 16;
   s->fn = kernel_for(dk, s->l2k, s->cm, c->l1_type);
+  if (!s->fn) {  // experiment libraries (make KSET=...) carry a subset of the variants
+    set_last_error("kernel variant dk=%d l2=%d l0cap=%d l1=%d is not built into this library", dk, s->l2k, s->cm, c->l1_type);
+    return MLMQ_EENGINE;
+  }
   const int es = dk == DK_U64 ? 16 : 8;
   const int L = c->lanes_per_group;
   s->batch_cap = std::max(c->block_size, 32);
