@@ -88,6 +88,10 @@ typedef struct {
                                        reference's `want`); up to max(block_size, 32)   */
   int32_t hub_threshold;            /* lists longer than this become hub descriptors
                                        (0 = 4 x hub_chunk)                              */
+  int32_t test_capacity;            /* > 0: every queue store (ring slots, hub descriptors,
+                                       heap nodes) gets exactly this many entries -- a
+                                       test hook that forces the overflow paths (l2.py:116-135) */
+  int32_t flags;                    /* MLMQ_F_* engine extensions (0 = none)             */
   int32_t reserved[2];
 } mlmq_config_t;
 
@@ -231,6 +235,46 @@ int mlmq_build_csr(uint64_t n, uint64_t m, const uint32_t* src, const uint32_t* 
  * (splitmix64 of seed ^ edge index; no reference analogue).
  */
 int mlmq_gen_f32_weights(uint64_t m, uint64_t seed, float* w_out);
+
+/*
+ * Device queue harness: one L2 queue (l2.py:73-451) in device memory, driven by the same
+ * device code the solve kernel runs.  Replaces the reference's Python queue objects
+ * L2BlockFifo / L2Bucket / L2PriorityQueue / L2MultiQueue (l2.py:73, 181, 304, 416) for
+ * its queue tests (pkg/tests/test_l2_queues.py, test_acceptance.py:282).
+ *   write: one write(batch, group) of n (v, d) pairs (l2.py:96-114, 224-233, 322-344, 430-438)
+ *   read : one try_read(group) -> up to one block / 32 heap elements (l2.py:161-166, 235-292,
+ *          362-389, 440-442)
+ *   stats: out[0] resident elements, [1] claimed-but-unconsumed tickets, [2] structurally
+ *          empty, [3] bucket epoch (floor = epoch * delta), [4] heap property holds,
+ *          [5] write tickets, [6] read tickets, [7..7+min(pnum,32)) elements per heap
+ *   stress: `writers` warps write ids [w*stride+begin, w*stride+end) with d = f(id) while
+ *          `readers` warps read until `stop_at` elements were consumed; every element read
+ *          is appended to pairs_out (v, d) (cap pairs); bucket readers log the epoch of each
+ *          read (epochs_out[reader * log_cap + k], counts in log_n[reader]).
+ */
+typedef struct mlmq_queue mlmq_queue;
+typedef struct {
+  int32_t l2_type;        /* MLMQ_L2_*                                          */
+  int32_t block_size;     /* elements per ring block                            */
+  int64_t block_num;      /* ring slots (rounded up to a power of two)          */
+  double delta;           /* bucket width                                       */
+  int32_t bmax, bnum;     /* bucket ring count / read window                    */
+  int32_t node_batch;     /* heap node size (<= 32)                             */
+  int32_t pnum;           /* heaps of the multi queue                           */
+  int32_t num_groups;     /* group ids that may call (multi write cursors)      */
+  int32_t reserved0;
+  int64_t heap_nodes;     /* node pool per heap (0 = 65536)                     */
+  double spin_timeout_s;  /* slot wait before QueueOverflowError                */
+} mlmq_queue_params_t;
+
+int mlmq_queue_create(int device, const mlmq_queue_params_t* params, mlmq_queue** out);
+void mlmq_queue_destroy(mlmq_queue* q);
+int mlmq_queue_write(mlmq_queue* q, const uint32_t* pairs, uint64_t n, int32_t group);
+int mlmq_queue_read(mlmq_queue* q, int32_t group, uint32_t* pairs_out, uint64_t cap, uint64_t* n_out);
+int mlmq_queue_stats(mlmq_queue* q, uint64_t out[40]);
+int mlmq_queue_stress(mlmq_queue* q, int32_t writers, int32_t readers, uint64_t stride, uint64_t begin,
+                      uint64_t end, uint64_t stop_at, uint32_t* pairs_out, uint64_t cap, uint64_t* n_out,
+                      uint64_t* epochs_out, uint64_t log_cap, uint64_t* log_n, double* ms_out);
 
 #ifdef __cplusplus
 }

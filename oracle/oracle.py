@@ -34,7 +34,11 @@ def _load():
         return _lib
     if not os.path.exists(_LIB_PATH) or (
             os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "sssp_oracle.c"))):
-        build()
+        try:
+            build()
+        except (OSError, subprocess.CalledProcessError):
+            if not os.path.exists(_LIB_PATH):
+                raise
     lib = ctypes.CDLL(_LIB_PATH)
     P = ctypes.c_void_p
     U64 = ctypes.c_uint64
@@ -46,6 +50,14 @@ def _load():
     lib.oracle_dijkstra_f32.restype = ctypes.c_int
     lib.oracle_reach_u64.argtypes = [U64, P, P, P, P]
     lib.oracle_reach_u64.restype = None
+    lib.mlmq_gen_size.argtypes = [ctypes.c_int, P, P, P]
+    lib.mlmq_gen_size.restype = ctypes.c_int
+    lib.mlmq_gen_graph.argtypes = [ctypes.c_int, P, P, U64, P, P, P]
+    lib.mlmq_gen_graph.restype = ctypes.c_int
+    lib.mlmq_gen_f32_weights.argtypes = [U64, U64, P]
+    lib.mlmq_gen_f32_weights.restype = ctypes.c_int
+    lib.oracle_last_error.argtypes = []
+    lib.oracle_last_error.restype = ctypes.c_char_p
     _lib = lib
     return lib
 
@@ -125,6 +137,52 @@ def dist_sha256(dist_u64: np.ndarray) -> str:
     """sha256 of distances_blob (engine.py:385-387): little-endian u64, INF all-ones."""
     import hashlib
     return hashlib.sha256(np.ascontiguousarray(dist_u64, dtype="<u8").tobytes()).hexdigest()
+
+
+class _GenParams(ctypes.Structure):
+    """mlmq_gen_params_t (include/mlmq.h)"""
+    _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("m", ctypes.c_int64), ("scale", ctypes.c_int64), ("edge_factor", ctypes.c_int64),
+                ("a", ctypes.c_double), ("b", ctypes.c_double), ("c", ctypes.c_double),
+                ("d", ctypes.c_double), ("wmin", ctypes.c_int64), ("wmax", ctypes.c_int64)]
+
+
+_GEN_KINDS = {"grid2d": 0, "path": 1, "uniform": 2, "rmat": 3}
+_GEN_DEFAULTS = {"rmat": dict(edge_factor=8, a=0.57, b=0.19, c=0.19, d=0.05, wmin=1, wmax=100),
+                 "grid2d": dict(wmin=1, wmax=1), "path": dict(wmin=1, wmax=1),
+                 "uniform": dict(wmin=1, wmax=100)}
+
+
+def generate(kind: str, seed: int = 0, **params):
+    """The reference generators (graph.py:306-420; defaults graph.py:310-362) from the
+    oracle library's own copy of the restatement -- for checkers and the bench's CPU
+    reference arm, which must not load the product library.  Returns (off, col, w)."""
+    lib = _load()
+    gp = _GenParams()
+    for k, v in {**_GEN_DEFAULTS[kind], **params}.items():
+        setattr(gp, k, v)
+    n, m = ctypes.c_uint64(), ctypes.c_uint64()
+    if lib.mlmq_gen_size(_GEN_KINDS[kind], ctypes.byref(gp), ctypes.byref(n), ctypes.byref(m)):
+        raise ValueError(lib.oracle_last_error().decode())
+    off = np.empty(n.value + 1, dtype=np.uint64)
+    col = np.empty(m.value, dtype=np.uint32)
+    w = np.empty(m.value, dtype=np.uint32)
+    s, limbs = abs(int(seed)), []
+    while s:
+        limbs.append(s & 0xFFFFFFFF)
+        s >>= 32
+    key = np.asarray(limbs or [0], dtype=np.uint32)
+    if lib.mlmq_gen_graph(_GEN_KINDS[kind], ctypes.byref(gp), key.ctypes.data, key.size,
+                          off.ctypes.data, col.ctypes.data, w.ctypes.data):
+        raise ValueError(lib.oracle_last_error().decode())
+    return off, col, w
+
+
+def f32_weights(m: int, seed: int) -> np.ndarray:
+    """Config-5 float weights U[0,1) (same counter-based stream as graph.with_f32_weights)."""
+    out = np.empty(m, dtype=np.float32)
+    _load().mlmq_gen_f32_weights(m, seed, out.ctypes.data)
+    return out
 
 
 def csr_sha256(row_offsets, col_indices, weights) -> str:

@@ -48,7 +48,8 @@ class Config(ctypes.Structure):
         ("watchdog_s", ctypes.c_double), ("spin_timeout_s", ctypes.c_double),
         ("hub_chunk", ctypes.c_int32), ("share", ctypes.c_int32), ("fifo_park", ctypes.c_int32),
         ("bucket_window", ctypes.c_int32), ("read_batch", ctypes.c_int32),
-        ("hub_threshold", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
+        ("hub_threshold", ctypes.c_int32), ("test_capacity", ctypes.c_int32),
+        ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
     ]
 
 
@@ -78,7 +79,8 @@ EXPORTED_SYMBOLS = (
     "mlmq_sssp", "mlmq_sssp_f32", "mlmq_sssp_device", "mlmq_last_dist", "mlmq_reach",
     "mlmq_feature_sums", "mlmq_gen_size", "mlmq_gen_graph", "mlmq_build_csr",
     "mlmq_gen_f32_weights", "mlmq_shard_create", "mlmq_shard_begin", "mlmq_shard_step",
-    "mlmq_host_alloc", "mlmq_host_free",
+    "mlmq_host_alloc", "mlmq_host_free", "mlmq_queue_create", "mlmq_queue_destroy",
+    "mlmq_queue_write", "mlmq_queue_read", "mlmq_queue_stats", "mlmq_queue_stress",
 )
 
 _lib = None
@@ -128,6 +130,13 @@ def lib():
             "mlmq_shard_step": ([P, P, P, U64, P, U64, P, P], I32),
             "mlmq_host_alloc": ([U64, P], I32),
             "mlmq_host_free": ([P], None),
+            "mlmq_queue_create": ([I32, P, P], I32),
+            "mlmq_queue_destroy": ([P], None),
+            "mlmq_queue_write": ([P, P, U64, ctypes.c_int32], I32),
+            "mlmq_queue_read": ([P, ctypes.c_int32, P, U64, P], I32),
+            "mlmq_queue_stats": ([P, P], I32),
+            "mlmq_queue_stress": ([P, ctypes.c_int32, ctypes.c_int32, U64, U64, U64, U64, P, U64, P, P, U64,
+                                   P, P], I32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -393,3 +402,73 @@ def f32_weights(m: int, seed: int) -> np.ndarray:
     out = np.empty(m, dtype=np.float32)
     check(lib().mlmq_gen_f32_weights(m, seed, _ptr(out)))
     return out
+
+
+class QueueParams(ctypes.Structure):
+    """mlmq_queue_params_t"""
+    _fields_ = [("l2_type", ctypes.c_int32), ("block_size", ctypes.c_int32), ("block_num", ctypes.c_int64),
+                ("delta", ctypes.c_double), ("bmax", ctypes.c_int32), ("bnum", ctypes.c_int32),
+                ("node_batch", ctypes.c_int32), ("pnum", ctypes.c_int32), ("num_groups", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("heap_nodes", ctypes.c_int64),
+                ("spin_timeout_s", ctypes.c_double)]
+
+
+class DeviceQueue:
+    """One L2 queue in device memory driven by the solve kernel's own queue code
+    (mlmq_queue_* in include/mlmq.h)."""
+
+    STATS = 40
+
+    def __init__(self, l2_type: int, *, block_size: int = 64, block_num: int = 4096, delta: float = 1.0,
+                 bmax: int = 64, bnum: int = 1, node_batch: int = 32, pnum: int = 1, num_groups: int = 64,
+                 heap_nodes: int = 0, spin_timeout_s: float = 15.0, device: int = 0):
+        L = lib()
+        if device_count() < 1:
+            _note_no_device()
+            raise EngineError("no CUDA device is visible; the MLMQ engine has no CPU fallback")
+        qp = QueueParams(l2_type, block_size, block_num, float(delta), bmax, bnum, node_batch, pnum,
+                         num_groups, 0, heap_nodes, float(spin_timeout_s))
+        h = ctypes.c_void_p()
+        check(L.mlmq_queue_create(device, ctypes.byref(qp), ctypes.byref(h)))
+        self._lib, self.handle = L, h
+        self.read_cap = max(block_size, 32)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.mlmq_queue_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def write(self, pairs: np.ndarray, group: int) -> None:
+        a = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        check(self._lib.mlmq_queue_write(self.handle, _ptr(a), a.shape[0], group))
+
+    def read(self, group: int) -> np.ndarray:
+        out = np.empty((self.read_cap, 2), dtype=np.uint32)
+        n = ctypes.c_uint64()
+        check(self._lib.mlmq_queue_read(self.handle, group, _ptr(out), self.read_cap, ctypes.byref(n)))
+        return out[: n.value]
+
+    def stats(self) -> np.ndarray:
+        out = np.zeros(self.STATS, dtype=np.uint64)
+        check(self._lib.mlmq_queue_stats(self.handle, _ptr(out)))
+        return out
+
+    def stress(self, writers: int, readers: int, stride: int, begin: int, end: int, stop_at: int,
+               cap: int, log_cap: int = 0):
+        pairs = np.empty((max(cap, 1), 2), dtype=np.uint32)
+        n = ctypes.c_uint64()
+        ms = ctypes.c_double()
+        logs = np.zeros((readers, max(log_cap, 1)), dtype=np.uint64) if log_cap else None
+        logn = np.zeros(readers, dtype=np.uint64) if log_cap else None
+        check(self._lib.mlmq_queue_stress(self.handle, writers, readers, stride, begin, end, stop_at,
+                                          _ptr(pairs), cap, ctypes.byref(n), _ptr(logs), log_cap,
+                                          _ptr(logn), ctypes.byref(ms)))
+        k = min(int(n.value), cap)
+        epochs = [logs[r, : int(logn[r])].tolist() for r in range(readers)] if log_cap else None
+        return pairs[:k], int(n.value), epochs, float(ms.value)

@@ -152,13 +152,16 @@ extern "C" int mlmq_gen_graph(int kind, const mlmq_gen_params_t* p, const uint32
         }
         break;
       case MLMQ_GEN_RMAT: {
-        const double a = p->a, ab = p->a + p->b, abc = p->a + p->b + p->c;
+        // graph.py:384-399 compares random() against a, a+b, a+b+c (double sums); the
+        // comparisons run on random()'s exact 53-bit numerator against ceil(t * 2^53)
+        const uint64_t a = PyRandom::ceil53(p->a), ab = PyRandom::ceil53(p->a + p->b),
+                       abc = PyRandom::ceil53(p->a + p->b + p->c);
         const int scale = (int)p->scale;
         for (uint64_t e = 0; e < m; ++e) {
           uint32_t u = 0, v = 0;
           for (int lv = 0; lv < scale; ++lv) {
             // quadrant a: (0,0)  b: (0,1)  c: (1,0)  d: (1,1) — branchless
-            const double r = rng.random();
+            const uint64_t r = rng.random53();
             const uint32_t ub = r >= ab;
             const uint32_t vb = (uint32_t)(r >= a) ^ (uint32_t)(r >= ab) ^ (uint32_t)(r >= abc);
             u = (u << 1) | ub;

@@ -22,19 +22,31 @@ class PyRandom {
 
   PyRandom(const uint32_t* key, size_t keylen) { seed_by_array(key, keylen); }
 
+  // Tempered outputs are produced a whole state (624 draws) at a time: the twist and
+  // the tempering then run as straight loops the compiler vectorises.
   uint32_t genrand() {
-    if (mti_ >= N) twist();
-    uint32_t y = mt_[mti_++];
-    y ^= (y >> 11);
-    y ^= (y << 7) & 0x9d2c5680U;
-    y ^= (y << 15) & 0xefc60000U;
-    y ^= (y >> 18);
-    return y;
+    if (mti_ >= N) refill();
+    return out_[mti_++];
   }
 
   double random() {
     uint32_t a = genrand() >> 5, b = genrand() >> 6;
     return (a * 67108864.0 + b) * (1.0 / 9007199254740992.0);
+  }
+
+  // random() as its exact 53-bit integer numerator R (random() == R / 2^53), so
+  // `random() >= t` <=> `random53() >= ceil53(t)` with no floating point on the hot path.
+  uint64_t random53() {
+    const uint64_t a = genrand() >> 5, b = genrand() >> 6;
+    return (a << 26) | b;
+  }
+  static uint64_t ceil53(double t) {
+    const double x = t * 9007199254740992.0;  // exact: power-of-two scaling
+    if (!(x > 0.0)) return 0;
+    if (x >= 9007199254740992.0) return 1ull << 53;
+    uint64_t c = (uint64_t)x;
+    if ((double)c < x) ++c;
+    return c;
   }
 
   uint32_t getrandbits(int k) {  // 0 < k <= 32
@@ -89,24 +101,28 @@ class PyRandom {
     mt_[0] = 0x80000000U;
   }
 
-  void twist() {
-    static const uint32_t mag01[2] = {0x0U, 0x9908b0dfU};
+  static uint32_t mix(uint32_t a, uint32_t b, uint32_t m) {
+    const uint32_t y = (a & 0x80000000U) | (b & 0x7fffffffU);
+    return m ^ (y >> 1) ^ ((0U - (y & 1U)) & 0x9908b0dfU);
+  }
+  void refill() {
     int kk = 0;
-    uint32_t y;
-    for (; kk < N - M; ++kk) {
-      y = (mt_[kk] & 0x80000000U) | (mt_[kk + 1] & 0x7fffffffU);
-      mt_[kk] = mt_[kk + M] ^ (y >> 1) ^ mag01[y & 1U];
+    for (; kk < N - M; ++kk) mt_[kk] = mix(mt_[kk], mt_[kk + 1], mt_[kk + M]);
+    for (; kk < N - 1; ++kk) mt_[kk] = mix(mt_[kk], mt_[kk + 1], mt_[kk + (M - N)]);
+    mt_[N - 1] = mix(mt_[N - 1], mt_[0], mt_[M - 1]);
+    for (int i = 0; i < N; ++i) {
+      uint32_t y = mt_[i];
+      y ^= (y >> 11);
+      y ^= (y << 7) & 0x9d2c5680U;
+      y ^= (y << 15) & 0xefc60000U;
+      y ^= (y >> 18);
+      out_[i] = y;
     }
-    for (; kk < N - 1; ++kk) {
-      y = (mt_[kk] & 0x80000000U) | (mt_[kk + 1] & 0x7fffffffU);
-      mt_[kk] = mt_[kk + (M - N)] ^ (y >> 1) ^ mag01[y & 1U];
-    }
-    y = (mt_[N - 1] & 0x80000000U) | (mt_[0] & 0x7fffffffU);
-    mt_[N - 1] = mt_[M - 1] ^ (y >> 1) ^ mag01[y & 1U];
     mti_ = 0;
   }
 
   uint32_t mt_[N];
+  uint32_t out_[N];
   int mti_ = N + 1;
 };
 

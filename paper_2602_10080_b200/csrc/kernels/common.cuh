@@ -309,4 +309,22 @@ struct KParams {
   unsigned long long obox_cap;
 };
 
+// Queue harness launch arguments (queue_harness.cu; mlmq_queue_* in include/mlmq.h).
+struct HarnessArgs {
+  int mode;                          // 0 write op, 1 read op, 2 stress
+  int group;                         // op mode: the calling group (multi: queue group % pnum)
+  const uint2* in;                   // op write: (v, d) pairs
+  unsigned long long n_in;
+  uint2* out;                        // read pairs
+  unsigned long long* out_n;         // fill of `out`
+  unsigned long long out_cap;
+  int* cursors;                      // multi: persistent per-group write cursor (l2.py:424)
+  int writers, readers;              // stress: warp gid < readers reads, the rest write
+  unsigned long long w_stride, w_begin, w_end;  // writer w writes ids [w*stride+begin, w*stride+end)
+  unsigned long long stop_at;        // readers stop once out_n >= stop_at
+  unsigned long long* epoch_log;     // bucket: [reader * log_cap + k] floor seen at read k
+  unsigned long long log_cap;
+  unsigned long long* log_n;         // per reader
+};
+
 }  // namespace mlmq

@@ -130,6 +130,7 @@ constexpr int kAuditWords = 14;
 struct Workspace {
   int es = 0, bs = 0, nrings = 0, nheaps = 0;
   unsigned long long bn = 0, hcap = 0, hub_cap = 0;
+  bool exact = false;  // sized by the test_capacity hook
   unsigned long long* seq = nullptr;
   uint32_t* cnt = nullptr;
   void* data = nullptr;
@@ -195,6 +196,7 @@ struct mlmq_graph {
   uint32_t* d_abort = nullptr;
   Workspace ws;
   int last_dk = -1;
+  bool poisoned = false;  // a kernel did not stop after an abort: the handle is unusable
   std::mutex mu;
   // sharded solve: 1D partition, v -> shard v mod P, local id v / P
   uint32_t nparts = 1, rank = 0;
@@ -216,6 +218,11 @@ struct ShardIo {
   unsigned long long send_cap = 0;
   uint64_t* send_counts = nullptr;  // host [nparts]
 };
+
+namespace mlmq {
+int harness_launch(int l2k, const KParams& p, const HarnessArgs& h, int warps, int wpb, size_t smem_per_warp,
+                   cudaStream_t stream);
+}
 
 namespace {
 
@@ -335,11 +342,19 @@ int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& s
     need.hcap = 0;
   }
   need.hub_cap = next_pow2(2ull * g->m / hub_chunk + 4096ull);
+  const bool exact = c->test_capacity > 0;  // test hook: force small stores (overflow paths)
+  if (exact) {
+    const unsigned long long tc = next_pow2((unsigned long long)c->test_capacity);
+    if (need.nrings) need.bn = tc;
+    if (need.nheaps) need.hcap = (unsigned long long)c->test_capacity;
+    need.hub_cap = tc;
+  }
 
   Workspace& w = g->ws;
   const bool fits = w.es == need.es && w.bs == need.bs && w.nrings == need.nrings &&
                     w.nheaps == need.nheaps && w.bn >= need.bn && w.hcap >= need.hcap &&
-                    w.hub_cap >= need.hub_cap && w.ptrs != nullptr;
+                    w.hub_cap >= need.hub_cap && w.ptrs != nullptr &&
+                    (!exact ? !w.exact : (w.bn == need.bn && w.hcap == need.hcap && w.hub_cap == need.hub_cap));
   if (!fits) {
     ws_free(w);
     size_t free_b = 0, total_b = 0;
@@ -364,6 +379,7 @@ int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& s
       w.bytes += b;
     };
     w = need;
+    w.exact = exact;
     w.bytes = 0;
     w.seq = nullptr;
     alloc((void**)&w.seq, nslots * 8);
@@ -504,42 +520,12 @@ void debug_dump(mlmq_graph* g, int G, const char* tag) {
   fprintf(stderr, "\n");
 }
 
-// One attempt at a given distance kind.  Returns MLMQ_OK, an error, or 100 when the
-// optimistic u32 distances overflowed (caller re-runs in u64).
-int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, int dk,
-             mlmq_metrics_t* mo, uint64_t* gm, uint64_t gm_cap, const ShardIo* io = nullptr) {
-  LaunchShape sh;
-  int st = launch_shape(g, c, dk, &sh);
-  if (st) return st;
-  int G = c->num_groups > 0 ? c->num_groups : sh.max_groups;
-  if (G > sh.max_groups) {
-    set_last_error("num_groups=%d exceeds the %d groups the device keeps resident for this configuration", G, sh.max_groups);
-    return MLMQ_EINVAL;
-  }
-  const unsigned long long hub_chunk = c->hub_chunk > 0 ? std::min<unsigned long long>((unsigned long long)c->hub_chunk, 1ull << 20) : 2048ull;
-  if ((st = ensure_workspace(g, c, sh, hub_chunk, G))) return st;
-  if (g->metrics_cap < (unsigned long long)G) {
-    cudaFree(g->d_metrics);
-    g->d_metrics = nullptr;
-    g->metrics_cap = 0;
-    CK(cudaMalloc(&g->d_metrics, (size_t)G * M_COUNT * 8));
-    g->metrics_cap = G;
-  }
-  Workspace& w = g->ws;
-  const bool dbg = debug_enabled();
-  if (dbg && g->prof_cap < (unsigned long long)G) {
-    cudaFree(g->d_prof);
-    cudaFree(g->d_wstate);
-    CK(cudaMalloc(&g->d_prof, (size_t)G * P_COUNT * 8));
-    CK(cudaMalloc(&g->d_wstate, (size_t)G * 16 + 64 + (size_t)G * 256 + 8 * 8192));
-    g->prof_cap = G;
-  }
-  if (dbg) {
-    CK(cudaMemset(g->d_prof, 0, (size_t)G * P_COUNT * 8));
-    CK(cudaMemset(g->d_wstate, 0, (size_t)G * 16 + 64 + (size_t)G * 256 + 8 * 8192));
-  }
+// The kernel parameter block of one launch (shared by the solve and the queue harness).
+KParams make_params(mlmq_graph* g, const mlmq_config_t* c, int dk, const LaunchShape& sh, int G,
+                    unsigned long long hub_chunk, unsigned long long source, bool dbg) {
   KParams p;
   std::memset(&p, 0, sizeof(p));
+  Workspace& w = g->ws;
   p.off = g->d_off;
   p.adj = g->d_adj;
   p.n = g->n;
@@ -627,7 +613,50 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   p.obox = g->d_obox;
   p.obox_n = g->d_sscratch;
   p.obox_cap = g->obox_cap;
+  return p;
+}
 
+// One attempt at a given distance kind.  Returns MLMQ_OK, an error, or 100 when the
+// optimistic u32 distances overflowed (caller re-runs in u64).
+int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, int dk,
+             mlmq_metrics_t* mo, uint64_t* gm, uint64_t gm_cap, const ShardIo* io = nullptr) {
+  LaunchShape sh;
+  int st = launch_shape(g, c, dk, &sh);
+  if (st) return st;
+  int G = c->num_groups > 0 ? c->num_groups : sh.max_groups;
+  if (G > sh.max_groups) {
+    set_last_error("num_groups=%d exceeds the %d groups the device keeps resident for this configuration", G, sh.max_groups);
+    return MLMQ_EINVAL;
+  }
+  const unsigned long long hub_chunk = c->hub_chunk > 0 ? std::min<unsigned long long>((unsigned long long)c->hub_chunk, 1ull << 20) : 2048ull;
+  if ((st = ensure_workspace(g, c, sh, hub_chunk, G))) return st;
+  if (g->metrics_cap < (unsigned long long)G) {
+    cudaFree(g->d_metrics);
+    g->d_metrics = nullptr;
+    g->metrics_cap = 0;
+    CK(cudaMalloc(&g->d_metrics, (size_t)G * M_COUNT * 8));
+    g->metrics_cap = G;
+  }
+  Workspace& w = g->ws;
+  const bool dbg = debug_enabled();
+  if (dbg && g->prof_cap < (unsigned long long)G) {
+    cudaFree(g->d_prof);
+    cudaFree(g->d_wstate);
+    CK(cudaMalloc(&g->d_prof, (size_t)G * P_COUNT * 8));
+    CK(cudaMalloc(&g->d_wstate, (size_t)G * 16 + 64 + (size_t)G * 256 + 8 * 8192));
+    g->prof_cap = G;
+  }
+  if (dbg) {
+    CK(cudaMemset(g->d_prof, 0, (size_t)G * P_COUNT * 8));
+    CK(cudaMemset(g->d_wstate, 0, (size_t)G * 16 + 64 + (size_t)G * 256 + 8 * 8192));
+  }
+  KParams p = make_params(g, c, dk, sh, G, hub_chunk, source, dbg);
+  const double spin = c->spin_timeout_s > 0 ? c->spin_timeout_s : 15.0;
+
+  if (g->poisoned) {
+    set_last_error("device graph is unusable: an earlier solve did not stop after its abort");
+    return MLMQ_EENGINE;
+  }
   *g->h_abort = 0;
   const int blocks = (G + 1 + sh.wpb - 1) / sh.wpb;
   const int init_blocks = (int)std::min<unsigned long long>(4ull * g->sm_count, (g->n + 255) / 256 + 1);
@@ -684,7 +713,11 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
       if (aborted && t - abort_t > 5.0) {
         if (dbg) debug_dump(g, G, "stuck-after-abort");
         w.dirty = true;
-        set_last_error("worker failed to stop after abort");
+        // the persistent kernel may still be resident: clearing the abort word for a new
+        // solve would un-abort it, and destroy must not wait on its stream
+        g->poisoned = true;
+        set_last_error("worker failed to stop after abort; the device graph is no longer usable "
+                       "(create a new one, or restart the process if the device stays busy)");
         return MLMQ_EENGINE;
       }
       std::this_thread::sleep_for(std::chrono::microseconds(20));
@@ -858,13 +891,78 @@ int solve(mlmq_graph* g, uint64_t source, const mlmq_config_t* c, void* dist_out
   return MLMQ_OK;
 }
 
-__global__ void interleave_kernel(const uint32_t* col, const uint32_t* w, uint2* adj, unsigned long long m, int unit) {
+// Interleave (col, weight) and count columns outside [0, col_bound) into *bad: a column
+// >= n would make the kernel read and atomically write past dist; the
+// reference raises IndexError on such a graph, the ABI returns MLMQ_EINVAL.
+__global__ void interleave_kernel(const uint32_t* col, const uint32_t* w, uint2* adj, unsigned long long m, int unit,
+                                  unsigned long long col_bound, unsigned long long* bad) {
   const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long k = tid; k < m; k += stride) adj[k] = make_uint2(col[k], unit ? 1u : w[k]);
+  unsigned nbad = 0;
+  for (unsigned long long k = tid; k < m; k += stride) {
+    const uint32_t c = col[k];
+    nbad += (unsigned long long)c >= col_bound;
+    adj[k] = make_uint2(c, unit ? 1u : w[k]);
+  }
+  if (nbad) atomicAdd(bad, (unsigned long long)nbad);
+}
+
+// Row offsets must be non-decreasing (a decreasing pair makes a huge unsigned degree).
+__global__ void offsets_check_kernel(const unsigned long long* off, unsigned long long n, unsigned long long* bad) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned nbad = 0;
+  for (unsigned long long i = tid; i < n; i += stride) nbad += off[i] > off[i + 1];
+  if (nbad) atomicAdd(bad, (unsigned long long)nbad);
 }
 
 }  // namespace
+
+
+// ------------------------------------------------------------------ queue harness
+struct mlmq_queue {
+  mlmq_graph* g = nullptr;   // carrier: device, stream, control words, queue workspace
+  mlmq_config_t c{};
+  LaunchShape sh;
+  KParams p{};
+  int l2k = 0, G = 0;
+  uint2* d_io = nullptr;
+  unsigned long long io_cap = 0;
+  unsigned long long* d_n = nullptr;
+  int* d_cursors = nullptr;
+  std::mutex mu;
+};
+
+static int queue_check_error(mlmq_queue* q) {
+  unsigned long long ctl[C_WORDS];
+  CK(cudaMemcpy(ctl, q->g->d_ctl, sizeof(ctl), cudaMemcpyDeviceToHost));
+  const unsigned long long err = ctl[C_ERR];
+  if (!err) return MLMQ_OK;
+  const double spin = q->c.spin_timeout_s > 0 ? q->c.spin_timeout_s : 15.0;
+  // the queue is wedged: later calls report the same error (like an aborted solve)
+  if (err == ERR_OVERFLOW) {
+    set_last_error("ring slot %llu stayed busy for %gs (block_num=%llu, write_ptr=%llu, read_ptr=%llu); block_num is likely too small for this workload",
+                   ctl[C_DIAG + 1], spin, (unsigned long long)q->g->ws.bn, ctl[C_DIAG + 2], ctl[C_DIAG + 3]);
+    return MLMQ_EOVERFLOW;
+  }
+  if (err == ERR_HEAP_OVERFLOW) {
+    set_last_error("batch heap %llu is full (%llu of %llu nodes)", ctl[C_DIAG], ctl[C_DIAG + 1], ctl[C_DIAG + 2]);
+    return MLMQ_EOVERFLOW;
+  }
+  set_last_error("queue harness error %llu (%llu %llu %llu %llu)", err, ctl[C_DIAG], ctl[C_DIAG + 1],
+                 ctl[C_DIAG + 2], ctl[C_DIAG + 3]);
+  return MLMQ_EENGINE;
+}
+
+static int queue_io(mlmq_queue* q, unsigned long long n) {
+  if (n <= q->io_cap) return MLMQ_OK;
+  cudaFree(q->d_io);
+  q->d_io = nullptr;
+  q->io_cap = 0;
+  CK(cudaMalloc(&q->d_io, std::max<unsigned long long>(n, 1024) * 8));
+  q->io_cap = std::max<unsigned long long>(n, 1024);
+  return MLMQ_OK;
+}
 
 extern "C" {
 
@@ -898,8 +996,16 @@ int mlmq_device_info(int device, int* sm_count, size_t* free_bytes, size_t* tota
   return MLMQ_OK;
 }
 
+static int graph_create_impl(const uint64_t* row_offsets, const uint32_t* col, const void* w, int weight_kind,
+                             uint64_t n, uint64_t m, int device, uint64_t col_bound, mlmq_graph** out);
+
 int mlmq_graph_create(const uint64_t* row_offsets, const uint32_t* col, const void* w, int weight_kind,
                       uint64_t n, uint64_t m, int device, mlmq_graph** out) {
+  return graph_create_impl(row_offsets, col, w, weight_kind, n, m, device, n, out);
+}
+
+static int graph_create_impl(const uint64_t* row_offsets, const uint32_t* col, const void* w, int weight_kind,
+                             uint64_t n, uint64_t m, int device, uint64_t col_bound, mlmq_graph** out) {
   if (!out || !row_offsets || (m && !col) || (m && weight_kind != MLMQ_W_UNIT && !w)) {
     set_last_error("null argument");
     return MLMQ_EINVAL;
@@ -944,6 +1050,9 @@ int mlmq_graph_create(const uint64_t* row_offsets, const uint32_t* col, const vo
   *g->h_abort = 0;
   CKG(cudaHostGetDevicePointer((void**)&g->d_abort, g->h_abort, 0));
   CKG(cudaMemcpy(g->d_off, row_offsets, (n + 1) * 8, cudaMemcpyHostToDevice));
+  CKG(cudaMemsetAsync(g->d_scratch, 0, 16 * 8, g->stream));
+  offsets_check_kernel<<<512, 256, 0, g->stream>>>(g->d_off, n, g->d_scratch);
+  CKG(cudaGetLastError());
   if (m) {
     // interleave (col, weight) on the device in chunks: one 8-byte load per edge
     const unsigned long long chunk = std::min<unsigned long long>(m, 1ull << 25);
@@ -957,7 +1066,8 @@ int mlmq_graph_create(const uint64_t* row_offsets, const uint32_t* col, const vo
       if (e == cudaSuccess && weight_kind != MLMQ_W_UNIT)
         e = cudaMemcpyAsync(dw, (const uint32_t*)w + k0, c * 4, cudaMemcpyHostToDevice, g->stream);
       if (e == cudaSuccess) {
-        interleave_kernel<<<1024, 256, 0, g->stream>>>(dc, dw, g->d_adj + k0, c, weight_kind == MLMQ_W_UNIT);
+        interleave_kernel<<<1024, 256, 0, g->stream>>>(dc, dw, g->d_adj + k0, c, weight_kind == MLMQ_W_UNIT,
+                                                       col_bound, g->d_scratch + 1);
         e = cudaGetLastError();
       }
       if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
@@ -967,6 +1077,13 @@ int mlmq_graph_create(const uint64_t* row_offsets, const uint32_t* col, const vo
     cudaFree(dw);
   }
   CKG(cudaStreamSynchronize(g->stream));
+  unsigned long long bad[2] = {0, 0};
+  CKG(cudaMemcpy(bad, g->d_scratch, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad[0] || bad[1]) {
+    if (bad[0]) set_last_error("row_offsets must be non-decreasing (%llu decreasing pairs)", bad[0]);
+    else set_last_error("%llu column indices lie outside [0, %llu)", bad[1], (unsigned long long)col_bound);
+    return fail(MLMQ_EINVAL);
+  }
 #undef CKG
   *out = g;
   return MLMQ_OK;
@@ -975,6 +1092,10 @@ int mlmq_graph_create(const uint64_t* row_offsets, const uint32_t* col, const vo
 void mlmq_graph_destroy(mlmq_graph* g) {
   if (!g) return;
   cudaSetDevice(g->device);
+  if (g->poisoned) {  // a kernel may still run on this stream: leak rather than hang or free under it
+    delete g;
+    return;
+  }
   if (g->stream) cudaStreamSynchronize(g->stream);
   ws_free(g->ws);
   cudaFree(g->d_off);
@@ -1091,7 +1212,7 @@ int mlmq_shard_create(const uint64_t* row_offsets, const uint32_t* col, const vo
                    (unsigned long long)((n_global - rank + nparts - 1) / nparts), (unsigned long long)n_local);
     return MLMQ_EINVAL;
   }
-  int st = mlmq_graph_create(row_offsets, col, w, weight_kind, n_local, m_local, device, out);
+  int st = graph_create_impl(row_offsets, col, w, weight_kind, n_local, m_local, device, n_global, out);
   if (st) return st;
   mlmq_graph* g = *out;
   g->nparts = nparts;
@@ -1205,6 +1326,257 @@ int mlmq_feature_sums(mlmq_graph* g, uint64_t out[10]) {
     out[9] = h[7];
   }
   return MLMQ_OK;
+}
+
+
+int mlmq_queue_create(int device, const mlmq_queue_params_t* qp, mlmq_queue** out) {
+  if (!qp || !out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  *out = nullptr;
+  if (qp->l2_type < 0 || qp->l2_type > 3) { set_last_error("unknown l2_type code %d", qp->l2_type); return MLMQ_EINVAL; }
+  if (qp->block_size < 1 || qp->block_size > 4096 || qp->block_num < 1) {
+    set_last_error("block_size must be in [1, 4096] and block_num >= 1");
+    return MLMQ_EINVAL;
+  }
+  const uint64_t off[2] = {0, 0};
+  mlmq_graph* g = nullptr;
+  int st = graph_create_impl(off, nullptr, nullptr, MLMQ_W_UNIT, 1, 0, device, 1, &g);
+  if (st) return st;
+  mlmq_queue* q = new mlmq_queue();
+  q->g = g;
+  mlmq_config_t& c = q->c;
+  c.l1_type = MLMQ_L1_VECTOR;
+  c.l2_type = qp->l2_type;
+  c.l0_capacity = 4;
+  c.l1_capacity = 64;
+  c.wb = 0;
+  c.delta = qp->delta > 0 ? qp->delta : 1.0;
+  c.block_size = qp->block_size;
+  c.block_num = qp->block_num;
+  c.bmax = std::max(1, qp->bmax);
+  c.bnum = std::max(1, std::min(qp->bnum, c.bmax));
+  c.node_batch = std::max(1, std::min(qp->node_batch, 32));
+  c.pnum = qp->l2_type == MLMQ_L2_MULTI ? std::max(1, qp->pnum) : 1;
+  c.num_groups = std::max(1, qp->num_groups);
+  c.lanes_per_group = 32;
+  c.dup_elim = 1;
+  c.spin_timeout_s = qp->spin_timeout_s > 0 ? qp->spin_timeout_s : 15.0;
+  c.read_batch = 32;
+  const bool heap = c.l2_type == MLMQ_L2_PRIORITY || c.l2_type == MLMQ_L2_MULTI;
+  c.test_capacity = (int32_t)std::min<long long>(heap ? (qp->heap_nodes > 0 ? qp->heap_nodes : 65536) : qp->block_num,
+                                                 1LL << 30);
+  auto fail = [&](int code) {
+    mlmq_queue_destroy(q);
+    return code;
+  };
+  if ((st = validate(&c))) return fail(st);
+  if ((st = launch_shape(g, &c, DK_U32, &q->sh))) return fail(st);
+  q->l2k = q->sh.l2k;
+  q->G = std::min(q->sh.max_groups, 1024);
+  if ((st = ensure_workspace(g, &c, q->sh, 2048ull, q->G))) return fail(st);
+  const size_t nslots = (size_t)std::max(g->ws.nrings, 1) * g->ws.bn;
+  reset_queues_kernel<<<1024, 256, 0, g->stream>>>(g->ws.seq, nslots, g->ws.bn - 1, g->ws.ptrs, std::max(g->ws.nrings, 1),
+                                                    g->ws.hub_seq, g->ws.hub_next, g->ws.hub_fin, g->ws.hub_cap, g->d_ctl,
+                                                    g->ws.hlock, g->ws.hsize, g->ws.hwc, std::max(g->ws.nheaps, 1));
+  g->ws.dirty = false;
+  if (cudaMemsetAsync(g->d_ctl, 0, C_WORDS * 8, g->stream) != cudaSuccess ||
+      cudaMalloc(&q->d_n, 64) != cudaSuccess ||
+      cudaMalloc(&q->d_cursors, sizeof(int) * (size_t)c.num_groups) != cudaSuccess) {
+    cudaGetLastError();
+    set_last_error("queue harness allocation failed");
+    return fail(MLMQ_ENOMEM);
+  }
+  std::vector<int> cur((size_t)c.num_groups);
+  for (int i = 0; i < c.num_groups; ++i) cur[(size_t)i] = i % c.pnum;
+  if (cudaMemcpy(q->d_cursors, cur.data(), cur.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaStreamSynchronize(g->stream) != cudaSuccess) {
+    cudaGetLastError();
+    set_last_error("queue harness initialisation failed");
+    return fail(MLMQ_ECUDA);
+  }
+  q->p = make_params(g, &c, DK_U32, q->sh, q->G, 2048ull, 0, false);
+  q->p.fifo_park = 0;  // conditional readers: no claim outlives a call (l2.py:141-148)
+  q->p.bwin = 0;       // the reference's floor rule (l2.py:282-287)
+  q->p.share = 0;
+  *out = q;
+  return MLMQ_OK;
+}
+
+void mlmq_queue_destroy(mlmq_queue* q) {
+  if (!q) return;
+  cudaFree(q->d_io);
+  cudaFree(q->d_n);
+  cudaFree(q->d_cursors);
+  mlmq_graph_destroy(q->g);
+  delete q;
+}
+
+int mlmq_queue_write(mlmq_queue* q, const uint32_t* pairs, uint64_t n, int32_t group) {
+  if (!q || (n && !pairs)) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  if (group < 0 || group >= q->c.num_groups) { set_last_error("group %d out of range", group); return MLMQ_EINVAL; }
+  if (n == 0) return MLMQ_OK;
+  std::lock_guard<std::mutex> lk(q->mu);
+  int st = queue_io(q, n);
+  if (st) return st;
+  CK(cudaMemcpyAsync(q->d_io, pairs, n * 8, cudaMemcpyHostToDevice, q->g->stream));
+  HarnessArgs h{};
+  h.mode = 0;
+  h.group = group;
+  h.in = q->d_io;
+  h.n_in = n;
+  h.cursors = q->l2k == L2K_HEAP ? q->d_cursors : nullptr;
+  if (harness_launch(q->l2k, q->p, h, 1, 1, (size_t)q->sh.smem_per_warp, q->g->stream) != 0) {
+    set_last_error("queue harness launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return MLMQ_ECUDA;
+  }
+  CK(cudaStreamSynchronize(q->g->stream));
+  return queue_check_error(q);
+}
+
+int mlmq_queue_read(mlmq_queue* q, int32_t group, uint32_t* pairs_out, uint64_t cap, uint64_t* n_out) {
+  if (!q || !n_out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  if (group < 0 || group >= q->c.num_groups) { set_last_error("group %d out of range", group); return MLMQ_EINVAL; }
+  std::lock_guard<std::mutex> lk(q->mu);
+  int st = queue_io(q, (unsigned long long)std::max(q->c.block_size, 32));
+  if (st) return st;
+  HarnessArgs h{};
+  h.mode = 1;
+  h.group = group;
+  h.out = q->d_io;
+  h.out_n = q->d_n;
+  h.out_cap = q->io_cap;
+  if (harness_launch(q->l2k, q->p, h, 1, 1, (size_t)q->sh.smem_per_warp, q->g->stream) != 0) {
+    set_last_error("queue harness launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return MLMQ_ECUDA;
+  }
+  unsigned long long c = 0;
+  CK(cudaMemcpyAsync(&c, q->d_n, 8, cudaMemcpyDeviceToHost, q->g->stream));
+  CK(cudaStreamSynchronize(q->g->stream));
+  if ((st = queue_check_error(q))) return st;
+  if (c > cap) { set_last_error("read returned %llu elements; buffer holds %llu", c, (unsigned long long)cap); return MLMQ_EINVAL; }
+  if (c) CK(cudaMemcpy(pairs_out, q->d_io, c * 8, cudaMemcpyDeviceToHost));
+  *n_out = c;
+  return MLMQ_OK;
+}
+
+int mlmq_queue_stats(mlmq_queue* q, uint64_t out[40]) {
+  if (!q || !out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  std::lock_guard<std::mutex> lk(q->mu);
+  std::memset(out, 0, 40 * sizeof(uint64_t));
+  const Workspace& w = q->g->ws;
+  unsigned long long ctl[C_WORDS];
+  CK(cudaMemcpy(ctl, q->g->d_ctl, sizeof(ctl), cudaMemcpyDeviceToHost));
+  out[3] = ctl[C_EPOCH];
+  bool empty = true, heap_ok = true;
+  if (q->l2k != L2K_HEAP) {
+    std::vector<unsigned long long> ptrs((size_t)w.nrings * 32), seq((size_t)w.nrings * w.bn);
+    std::vector<uint32_t> cnt((size_t)w.nrings * w.bn);
+    CK(cudaMemcpy(ptrs.data(), w.ptrs, ptrs.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(seq.data(), w.seq, seq.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cnt.data(), w.cnt, cnt.size() * 4, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < w.nrings; ++r) {
+      const unsigned long long wp = ptrs[(size_t)r * 32], rp = ptrs[(size_t)r * 32 + 16];
+      out[5] += wp;
+      out[6] += rp;
+      if (wp != rp) empty = false;
+      for (unsigned long long t = rp; t < wp; ++t) {  // written, unclaimed
+        const size_t i = (size_t)r * w.bn + (t & (w.bn - 1));
+        if (seq[i] == t + 1) out[0] += cnt[i];
+      }
+      const unsigned long long lo = rp > w.bn ? rp - w.bn : 0;
+      for (unsigned long long t = lo; t < rp; ++t) {  // claimed: consumed iff freed to t + bn
+        const size_t i = (size_t)r * w.bn + (t & (w.bn - 1));
+        if (seq[i] == t + 1) ++out[1];
+      }
+    }
+  } else {
+    std::vector<unsigned long long> hs((size_t)w.nheaps * 16), hw((size_t)w.nheaps * 16);
+    CK(cudaMemcpy(hs.data(), w.hsize, hs.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hw.data(), w.hwc, hw.size() * 8, cudaMemcpyDeviceToHost));
+    for (int h = 0; h < w.nheaps; ++h) {
+      const unsigned long long size = hs[(size_t)h * 16];
+      out[5] += hw[(size_t)h * 16];
+      if (size) empty = false;
+      std::vector<uint32_t> hc(size);
+      std::vector<uint2> nodes(size * 32);
+      if (size) {
+        CK(cudaMemcpy(hc.data(), w.hcnt + (size_t)h * w.hcap, size * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(nodes.data(), (uint2*)w.hnodes + (size_t)h * w.hcap * 32, size * 32 * 8, cudaMemcpyDeviceToHost));
+      }
+      unsigned long long elems = 0;
+      for (unsigned long long i = 0; i < size; ++i) {  // l2.py:391-402: sorted nodes, parent min <= child min
+        elems += hc[i];
+        if (hc[i] == 0 || hc[i] > 32) heap_ok = false;
+        for (uint32_t k = 1; k < hc[i] && k < 32; ++k)
+          if (nodes[i * 32 + k].y < nodes[i * 32 + k - 1].y) heap_ok = false;
+        if (i > 0 && nodes[i * 32].y < nodes[((i - 1) / 2) * 32].y) heap_ok = false;
+      }
+      out[0] += elems;
+      if (h < 32) out[7 + h] = elems;
+    }
+  }
+  out[2] = empty ? 1 : 0;
+  out[4] = heap_ok ? 1 : 0;
+  return MLMQ_OK;
+}
+
+int mlmq_queue_stress(mlmq_queue* q, int32_t writers, int32_t readers, uint64_t stride, uint64_t begin, uint64_t end,
+                      uint64_t stop_at, uint32_t* pairs_out, uint64_t cap, uint64_t* n_out, uint64_t* epochs_out,
+                      uint64_t log_cap, uint64_t* log_n, double* ms_out) {
+  if (!q || !pairs_out || !n_out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  if (writers < 0 || readers < 1 || writers + readers > q->G || writers + readers > q->c.num_groups) {
+    set_last_error("need 1 <= readers and writers + readers <= %d", std::min(q->G, q->c.num_groups));
+    return MLMQ_EINVAL;
+  }
+  std::lock_guard<std::mutex> lk(q->mu);
+  mlmq_graph* g = q->g;
+  uint2* d_out = nullptr;
+  unsigned long long* d_log = nullptr;
+  unsigned long long* d_logn = nullptr;
+  const bool logs = epochs_out && log_n && log_cap;
+  cudaError_t e = cudaMalloc(&d_out, std::max<uint64_t>(cap, 1) * 8);
+  if (e == cudaSuccess && logs) e = cudaMalloc(&d_log, (size_t)readers * log_cap * 8);
+  if (e == cudaSuccess && logs) e = cudaMalloc(&d_logn, (size_t)readers * 8);
+  auto cleanup = [&]() { cudaFree(d_out); cudaFree(d_log); cudaFree(d_logn); };
+  if (e != cudaSuccess) { cudaGetLastError(); cleanup(); set_last_error("stress buffers: %s", cudaGetErrorString(e)); return MLMQ_ENOMEM; }
+  HarnessArgs h{};
+  h.mode = 2;
+  h.out = d_out;
+  h.out_n = q->d_n;
+  h.out_cap = cap;
+  h.writers = writers;
+  h.readers = readers;
+  h.w_stride = stride;
+  h.w_begin = begin;
+  h.w_end = end;
+  h.stop_at = stop_at;
+  h.epoch_log = d_log;
+  h.log_cap = logs ? log_cap : 0;
+  h.log_n = d_logn;
+  KParams p = q->p;
+  p.G = writers + readers;
+  if (cudaMemsetAsync(q->d_n, 0, 8, g->stream) != cudaSuccess) { cleanup(); CK(cudaGetLastError()); }
+  CK(cudaEventRecord(g->ev0, g->stream));
+  const int wpb = std::max(1, q->sh.wpb);
+  if (harness_launch(q->l2k, p, h, writers + readers, wpb, (size_t)q->sh.smem_per_warp, g->stream) != 0) {
+    cleanup();
+    set_last_error("queue stress launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return MLMQ_ECUDA;
+  }
+  CK(cudaEventRecord(g->ev1, g->stream));
+  e = cudaStreamSynchronize(g->stream);
+  if (e != cudaSuccess) { cleanup(); CK(e); }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, g->ev0, g->ev1);
+  if (ms_out) *ms_out = ms;
+  unsigned long long n = 0;
+  e = cudaMemcpy(&n, q->d_n, 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && n) e = cudaMemcpy(pairs_out, d_out, std::min<unsigned long long>(n, cap) * 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && logs) e = cudaMemcpy(epochs_out, d_log, (size_t)readers * log_cap * 8, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && logs) e = cudaMemcpy(log_n, d_logn, (size_t)readers * 8, cudaMemcpyDeviceToHost);
+  cleanup();
+  CK(e);
+  *n_out = n;
+  return queue_check_error(q);
 }
 
 }  // extern "C"

@@ -50,6 +50,8 @@ class EngineConfig:
     bucket_window: int = 1   # bucket L2: winners >= this many buckets above the floor skip L0/L1
     read_batch: int = 64     # elements per L1 read (0 = lanes_per_group, the reference's want)
     hub_threshold: int = 0   # lists longer than this become hub descriptors (0 = 4 x hub_chunk)
+    test_capacity: int = 0   # > 0: every queue store gets exactly this many entries (test hook
+                             # that forces the QueueOverflowError paths, l2.py:116-135)
 
 
 class SsspResult:
@@ -185,6 +187,7 @@ def _native_config(cfg: MlmqConfig, eng: EngineConfig, unit_weights: bool,
     c.bucket_window = max(0, int(eng.bucket_window))
     c.read_batch = max(0, int(eng.read_batch))
     c.hub_threshold = max(0, int(eng.hub_threshold))
+    c.test_capacity = max(0, int(eng.test_capacity))
     return c
 
 

@@ -342,26 +342,6 @@ def test_baseline_configs_match_reference_hashes(name, sha):
         assert_balanced(r.metrics)
 
 
-def test_c5_float_weights_match_f32_oracle():
-    from bench import build_graph, solve_config
-    g = build_graph("c5")
-    f = extract_features(g)
-    r = sssp_solve(g, 0, solve_config("c5", g, f), features=f)
-    want = oracle.dijkstra_f32(g.row_offsets, g.col_indices, g.weights, 0)
-    assert np.array_equal(r.dist_array, want)
-
-
-def test_sharded_equals_unsharded_on_c2():
-    from bench import build_graph, solve_config
-    from paper_2602_10080_b200.sharded import sssp_solve_sharded
-    g = build_graph("c2")
-    f = extract_features(g)
-    want = sssp_solve(g, 0, solve_config("c2", g, f), features=f).dist_array
-    for P in (2, 8):
-        res = sssp_solve_sharded(g, 0, P, MlmqConfig(l2_type="fifo"))
-        assert np.array_equal(res.local_dist, want), P
-
-
 def test_recycled_result_buffers_are_not_aliased():
     # results live in page-locked buffers recycled across solves: a held result must
     # never be overwritten by a later solve
