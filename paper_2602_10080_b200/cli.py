@@ -208,8 +208,9 @@ def cmd_solve(args) -> int:
     d = res.dist_array
     reach = int(np.count_nonzero(np.isfinite(d))) if d.dtype == np.float32 else \
         int(np.count_nonzero(d != np.uint64(0xFFFFFFFFFFFFFFFF)))
-    out["device"] = {"kernel_ms": res.kernel_ms, "num_groups": res.native["num_groups"],
-                     "dist_bits": res.native["dist_bits"], "reached_vertices": reach}
+    if args.report_device:  # timing varies run to run: opt-in (test_cli.py:171-179)
+        out["device"] = {"kernel_ms": res.kernel_ms, "num_groups": res.native["num_groups"],
+                         "dist_bits": res.native["dist_bits"], "reached_vertices": reach}
     if g.num_vertices <= args.max_inline_distances:
         out["distances"] = _inline(d)
     else:
@@ -363,6 +364,8 @@ def build_parser() -> argparse.ArgumentParser:
         p.add_argument("--unit-weights", action="store_true")
         if name == "solve":
             p.add_argument("--max-inline-distances", type=int, default=MAX_INLINE)
+            p.add_argument("--report-device", action="store_true",
+                           help="add the device time / group count / distance width (B200 extension)")
         p.add_argument("--out")
         p.set_defaults(fn=fn)
 

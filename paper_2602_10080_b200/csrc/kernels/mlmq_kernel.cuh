@@ -29,6 +29,9 @@ struct Worker {
 #define MLMQ_U 4  // measured on B200 (C2): U=2 2.26 ms, 3 1.69, 4 1.64, 5 1.78, 6 1.88, 8 1.98, 12 2.82
 #endif
   static constexpr int U = MLMQ_U;  // edge slots per lane per step (U independent loads in flight)
+#ifndef MLMQ_PIPE
+#define MLMQ_PIPE 0  // 1: issue step k+1's adjacency loads before step k's checks (2U loads in flight)
+#endif
 
   const KParams& p;
   S* dist;
@@ -1370,7 +1373,14 @@ struct Worker {
   // ============================================================ relaxation
   // engine.py:201-220 per edge: nd = dist[u] + w; if nd < dist[v] and atomic-min
   // improves (core.py:205-213): emit (v, nd).
-  __device__ void relax_slots(bool (&act)[U], const unsigned long long (&kk)[U], const S (&du)[U]) {
+  // Split in two so the expansion loops can software-pipeline: the U adjacency loads of
+  // step k+1 are issued (adj_issue) before step k's dependent distance checks run
+  // (relax_loaded), so a warp keeps 2U independent DRAM loads in flight per lane.
+  __device__ __forceinline__ void adj_issue(const bool (&act)[U], const unsigned long long (&kk)[U], uint2 (&a)[U]) const {
+#pragma unroll
+    for (int j = 0; j < U; ++j) a[j] = act[j] ? __ldg(p.adj + kk[j]) : make_uint2(0u, 0u);
+  }
+  __device__ void relax_loaded(bool (&act)[U], const uint2 (&a)[U], const S (&du)[U]) {
     LOC();
     uint32_t v[U];
     S nd[U];
@@ -1380,9 +1390,8 @@ struct Worker {
       v[j] = 0;
       nd[j] = 0;
       if (act[j]) {
-        const uint2 a = __ldg(p.adj + kk[j]);
-        v[j] = a.x;
-        nd[j] = Tr::add(du[j], p.unit ? 1u : a.y, dist_ovf);
+        v[j] = a[j].x;
+        nd[j] = Tr::add(du[j], p.unit ? 1u : a[j].y, dist_ovf);
         ++c;
         if (nd[j] == (S)Tr::INF) act[j] = false;
       }
@@ -1416,6 +1425,11 @@ struct Worker {
     n_upd += (unsigned)upd;  // warp total, lane-replicated
     __syncwarp();
     if (outn >= L) flush_out(false);
+  }
+  __device__ void relax_slots(bool (&act)[U], const unsigned long long (&kk)[U], const S (&du)[U]) {
+    uint2 a[U];
+    adj_issue(act, kk, a);
+    relax_loaded(act, a, du);
   }
 
   // Sharded solve: this group's shard owns global vertices v with
@@ -1470,18 +1484,45 @@ struct Worker {
     S dus[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) dus[j] = du;
+    bool act[U];
+    unsigned long long kk[U];
+    uint2 a[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      kk[j] = lo + (unsigned long long)(j * 32 + lane);
+      act[j] = kk[j] < hi;
+    }
+#if MLMQ_PIPE
+    adj_issue(act, kk, a);
     for (unsigned long long k0 = lo; k0 < hi; k0 += 32 * U) {
       LOC();
-      bool act[U];
-      unsigned long long kk[U];
+      bool act2[U];
+      uint2 a2[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {  // next step's loads go out before this step's checks
+        kk[j] += 32 * U;
+        act2[j] = kk[j] < hi;
+      }
+      adj_issue(act2, kk, a2);
+      relax_loaded(act, a, dus);
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        LOC();
-        kk[j] = k0 + (unsigned long long)(j * 32 + lane);
+        act[j] = act2[j];
+        a[j] = a2[j];
+      }
+    }
+#else
+    for (unsigned long long k0 = lo; k0 < hi; k0 += 32 * U) {
+      LOC();
+      adj_issue(act, kk, a);
+      relax_loaded(act, a, dus);
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        kk[j] += 32 * U;
         act[j] = kk[j] < hi;
       }
-      relax_slots(act, kk, dus);
     }
+#endif
   }
 
   // Hub descriptors (new tier): one descriptor per hub list, split into
@@ -1631,6 +1672,40 @@ struct Worker {
   }
 
 
+  // One step of the flattened expansion: edge slot idx = e0 + j*32 + lane finds its
+  // owner row by a 5-step shuffle search over the warp's inclusive degree scan (all U
+  // searches unconditional so they interleave), then its adjacency load is issued.
+  __device__ __forceinline__ void expand_step(int e0, int total, int incl, unsigned long long base_e, S du,
+                                              bool (&act)[U], S (&dus)[U], uint2 (&a)[U]) {
+    if (e0 >= total) {  // warp-uniform: past the last step
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        act[j] = false;
+        dus[j] = 0;
+        a[j] = make_uint2(0u, 0u);
+      }
+      return;
+    }
+    const unsigned long long tq0 = pclk();
+    unsigned long long kk[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int idx = e0 + j * 32 + lane;
+      int o = 0;
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) {
+        const int probe = __shfl_sync(FULL, incl, o + s - 1);
+        if (probe <= idx) o += s;
+      }
+      const unsigned long long ob = __shfl_sync(FULL, base_e, o);
+      dus[j] = __shfl_sync(FULL, du, o);
+      act[j] = idx < total;
+      kk[j] = ob + (unsigned long long)idx;
+    }
+    pacc(P_SPINS, tq0);
+    adj_issue(act, kk, a);
+  }
+
   // engine.py:171-227 for one batch in shared memory
   __device__ void relax_batch(int nb) {
     LOC();
@@ -1700,34 +1775,40 @@ struct Worker {
       const int total = __shfl_sync(FULL, incl, 31);
       const int excl = incl - ds;
       const unsigned long long base_e = lo - (unsigned long long)excl;  // edge = base[owner] + slot
+#if MLMQ_PIPE
+      // step e0's owner search + adjacency loads are issued one step ahead
+      bool act[U];
+      S dus[U];
+      uint2 a[U];
+      expand_step(0, total, incl, base_e, du, act, dus, a);
       for (int e0 = 0; e0 < total; e0 += 32 * U) {
         LOC();
-        const unsigned long long tq0 = pclk();
-        bool act[U];
-        unsigned long long kk[U];
-        S dus[U];
+        const unsigned long long ts0 = pclk();
+        bool act2[U];
+        S dus2[U];
+        uint2 a2[U];
+        expand_step(e0 + 32 * U, total, incl, base_e, du, act2, dus2, a2);
+        relax_loaded(act, a, dus);
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-          LOC();
-          // all U rows unconditionally: the 8 independent 5-step shuffle searches
-          // interleave (a per-row branch would serialise them)
-          const int idx = e0 + j * 32 + lane;
-          int o = 0;
-#pragma unroll
-          for (int s = 16; s >= 1; s >>= 1) {
-            const int probe = __shfl_sync(FULL, incl, o + s - 1);
-            if (probe <= idx) o += s;
-          }
-          const unsigned long long ob = __shfl_sync(FULL, base_e, o);
-          dus[j] = __shfl_sync(FULL, du, o);
-          act[j] = idx < total;
-          kk[j] = ob + (unsigned long long)idx;
+          act[j] = act2[j];
+          dus[j] = dus2[j];
+          a[j] = a2[j];
         }
-        pacc(P_SPINS, tq0);
-        const unsigned long long ts0 = pclk();
-        relax_slots(act, kk, dus);
         pacc(P_STEPS, ts0);
       }
+#else
+      for (int e0 = 0; e0 < total; e0 += 32 * U) {
+        LOC();
+        const unsigned long long ts0 = pclk();
+        bool act[U];
+        S dus[U];
+        uint2 a[U];
+        expand_step(e0, total, incl, base_e, du, act, dus, a);
+        relax_loaded(act, a, dus);
+        pacc(P_STEPS, ts0);
+      }
+#endif
     }
     const unsigned long long tf0 = pclk();
     flush_out(true);

@@ -605,7 +605,9 @@ KParams make_params(mlmq_graph* g, const mlmq_config_t* c, int dk, const LaunchS
   p.share = c->share ? 1 : 0;
   p.fifo_park = (sh.l2k == L2K_FIFO && c->fifo_park) ? 1 : 0;
   p.bscratch = sh.bscratch;
-  p.bwin = (sh.l2k == L2K_BUCKET && c->bmax >= 3) ? std::max(0, c->bucket_window) : 0;
+  // a single group gains nothing from a managed floor and keeps the reference's
+  // deterministic one-group schedule (test_engine.py:141-148, test_cli.py:171-179)
+  p.bwin = (sh.l2k == L2K_BUCKET && c->bmax >= 3 && G > 1) ? std::max(0, c->bucket_window) : 0;
   p.nparts = (int)g->nparts;
   p.part_shift = g->shift;
   p.rank = g->rank;

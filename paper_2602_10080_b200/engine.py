@@ -47,7 +47,9 @@ class EngineConfig:
     device: int = 0
     share: bool = True       # eager write-back to L2 while groups idle (B200 extension)
     fifo_park: bool = True   # FIFO readers park on unconditional tickets
-    bucket_window: int = 1   # bucket L2: winners >= this many buckets above the floor skip L0/L1
+    bucket_window: int = -1  # bucket L2: winners >= this many buckets above the floor skip L0/L1;
+                             # -1 = auto: 1 (managed floor) with >= 64 groups, else 0 (the
+                             # reference's floor rule, l2.py:282-287)
     read_batch: int = 64     # elements per L1 read (0 = lanes_per_group, the reference's want)
     hub_threshold: int = 0   # lists longer than this become hub descriptors (0 = 4 x hub_chunk)
     test_capacity: int = 0   # > 0: every queue store gets exactly this many entries (test hook
@@ -184,7 +186,10 @@ def _native_config(cfg: MlmqConfig, eng: EngineConfig, unit_weights: bool,
     c.hub_chunk = int(eng.hub_chunk)
     c.share = 1 if eng.share else 0
     c.fifo_park = 1 if eng.fifo_park else 0
-    c.bucket_window = max(0, int(eng.bucket_window))
+    bw = int(eng.bucket_window)
+    if bw < 0:
+        bw = 1 if (cfg.num_groups is None or cfg.num_groups >= 64) else 0
+    c.bucket_window = bw
     c.read_batch = max(0, int(eng.read_batch))
     c.hub_threshold = max(0, int(eng.hub_threshold))
     c.test_capacity = max(0, int(eng.test_capacity))
