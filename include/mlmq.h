@@ -95,6 +95,9 @@ typedef struct {
   int32_t reserved[2];
 } mlmq_config_t;
 
+/* mlmq_config_t.flags */
+enum { MLMQ_F_PREFETCH_TARGETS = 1 /* prefetch row offsets of improved targets into L2 */ };
+
 /*
  * Aggregate counters; the first 11 fields follow core.py:142-154 (METRIC_FIELDS),
  * wall_time_us is core.py:176.  The rest are GPU-side extras kept outside the schema.
@@ -191,6 +194,9 @@ int mlmq_shard_create(const uint64_t* row_offsets, const uint32_t* col, const vo
                       uint64_t n_local, uint64_t m_local, uint64_t n_global, uint32_t rank,
                       uint32_t nparts, int device, mlmq_graph** out);
 int mlmq_shard_begin(mlmq_graph* g);
+/* The cudaStream_t the library runs g's kernels on (as void*), so a caller can order its
+ * own stream (NCCL's) against it with events instead of host synchronisation. */
+int mlmq_graph_stream(mlmq_graph* g, void** out);
 int mlmq_shard_step(mlmq_graph* g, const mlmq_config_t* cfg, const uint32_t* d_inbox, uint64_t n_in,
                     uint32_t* d_send, uint64_t send_cap, uint64_t* send_counts,
                     mlmq_metrics_t* metrics_out);
@@ -223,6 +229,15 @@ enum { MLMQ_GEN_GRID2D = 0, MLMQ_GEN_PATH = 1, MLMQ_GEN_UNIFORM = 2, MLMQ_GEN_RM
 int mlmq_gen_size(int kind, const mlmq_gen_params_t* p, uint64_t* n_out, uint64_t* m_out);
 int mlmq_gen_graph(int kind, const mlmq_gen_params_t* p, const uint32_t* key, uint64_t keylen,
                    uint64_t* row_offsets, uint32_t* col, uint32_t* w);
+
+/* One shard of a generated graph (sharded.py shard_csr layout): rows u with
+ * u % nparts == rank at local id u / nparts, global column ids, from the same RNG stream
+ * (each rank generates only its own slice: no rank holds the whole graph).  Call twice:
+ * first with col == NULL (fills row_offsets[n_local + 1] and *m_out), then with col / w
+ * of *m_out entries. */
+int mlmq_gen_shard(int kind, const mlmq_gen_params_t* p, const uint32_t* key, uint64_t keylen,
+                   uint32_t nparts, uint32_t rank, uint64_t* row_offsets, uint32_t* col, uint32_t* w,
+                   uint64_t* m_out);
 
 /* Stable CSR build from an edge list (graph.py:89-124 ordering; zero-weight self loops
  * dropped).  Returns m_kept via *m_out; caller allocates row_offsets[n+1], col[m], w[m]. */

@@ -77,8 +77,8 @@ EXPORTED_SYMBOLS = (
     "mlmq_abi_version", "mlmq_last_error", "mlmq_device_count", "mlmq_device_info",
     "mlmq_graph_create", "mlmq_graph_destroy", "mlmq_graph_device_bytes", "mlmq_auto_groups",
     "mlmq_sssp", "mlmq_sssp_f32", "mlmq_sssp_device", "mlmq_last_dist", "mlmq_reach",
-    "mlmq_feature_sums", "mlmq_gen_size", "mlmq_gen_graph", "mlmq_build_csr",
-    "mlmq_gen_f32_weights", "mlmq_shard_create", "mlmq_shard_begin", "mlmq_shard_step",
+    "mlmq_feature_sums", "mlmq_gen_size", "mlmq_gen_graph", "mlmq_gen_shard", "mlmq_build_csr",
+    "mlmq_gen_f32_weights", "mlmq_shard_create", "mlmq_shard_begin", "mlmq_shard_step", "mlmq_graph_stream",
     "mlmq_host_alloc", "mlmq_host_free", "mlmq_queue_create", "mlmq_queue_destroy",
     "mlmq_queue_write", "mlmq_queue_read", "mlmq_queue_stats", "mlmq_queue_stress",
 )
@@ -125,8 +125,10 @@ def lib():
             "mlmq_gen_graph": ([I32, P, P, U64, P, P, P], I32),
             "mlmq_build_csr": ([U64, U64, P, P, P, P, P, P, P], I32),
             "mlmq_gen_f32_weights": ([U64, U64, P], I32),
+            "mlmq_gen_shard": ([I32, P, P, U64, ctypes.c_uint32, ctypes.c_uint32, P, P, P, P], I32),
             "mlmq_shard_create": ([P, P, P, I32, U64, U64, U64, ctypes.c_uint32, ctypes.c_uint32, I32, P], I32),
             "mlmq_shard_begin": ([P], I32),
+            "mlmq_graph_stream": ([P, P], I32),
             "mlmq_shard_step": ([P, P, P, U64, P, U64, P, P], I32),
             "mlmq_host_alloc": ([U64, P], I32),
             "mlmq_host_free": ([P], None),
@@ -345,6 +347,12 @@ class DeviceShard(DeviceGraph):
     def begin(self) -> None:
         check(self._lib.mlmq_shard_begin(self.handle))
 
+    def stream_ptr(self) -> int:
+        """The library's CUDA stream for this shard (cudaStream_t as an int)."""
+        p = ctypes.c_void_p()
+        check(self._lib.mlmq_graph_stream(self.handle, ctypes.byref(p)))
+        return int(p.value or 0)
+
     def step(self, cfg: Config, inbox_ptr: int, n_in: int, send_ptr: int, send_cap: int):
         """One superstep; inbox/send are DEVICE pointers to (v, d) u32 pairs.  Returns
         (per-owner send counts, Metrics)."""
@@ -380,6 +388,28 @@ def generate(kind: str, seed: int, params: dict):
     check(L.mlmq_gen_graph(GEN_KINDS[kind], ctypes.byref(gp), _ptr(key), key.size,
                            _ptr(off), _ptr(col), _ptr(w)))
     return off, col, w
+
+
+def generate_shard(kind: str, seed: int, params: dict, nparts: int, rank: int):
+    """Rank's slice of a generated graph (rows v % nparts == rank at local id v // nparts,
+    global columns): (row_offsets u64, col u32, weights u32, n_global)."""
+    L = lib()
+    gp = GenParams()
+    for k, v in params.items():
+        setattr(gp, k, v)
+    n, m = ctypes.c_uint64(), ctypes.c_uint64()
+    check(L.mlmq_gen_size(GEN_KINDS[kind], ctypes.byref(gp), ctypes.byref(n), ctypes.byref(m)))
+    n_loc = (int(n.value) - rank + nparts - 1) // nparts
+    off = np.empty(n_loc + 1, dtype=np.uint64)
+    key = seed_key(seed)
+    mk = ctypes.c_uint64()
+    check(L.mlmq_gen_shard(GEN_KINDS[kind], ctypes.byref(gp), _ptr(key), key.size, nparts, rank, _ptr(off),
+                           None, None, ctypes.byref(mk)))
+    col = np.empty(mk.value, dtype=np.uint32)
+    w = np.empty(mk.value, dtype=np.uint32)
+    check(L.mlmq_gen_shard(GEN_KINDS[kind], ctypes.byref(gp), _ptr(key), key.size, nparts, rank, _ptr(off),
+                           _ptr(col), _ptr(w), ctypes.byref(mk)))
+    return off, col, w, int(n.value)
 
 
 def build_csr_native(n: int, src: np.ndarray, dst: np.ndarray, w: np.ndarray):

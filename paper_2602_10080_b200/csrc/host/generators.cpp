@@ -31,10 +31,20 @@ inline uint32_t draw_weight(PyRandom& rng, int64_t wmin, int64_t wmax) {
   return wmin == wmax ? (uint32_t)wmin : (uint32_t)rng.randint(wmin, wmax);
 }
 
+// Edge list of one shard: with nparts > 1 only edges whose source u satisfies
+// u % nparts == rank are kept, at local row u / nparts (columns stay global), so the
+// CSR built from it is exactly rank's slice of the full CSR (sharded.py shard_csr).
+// Zero-weight self loops are dropped here, on global ids (graph.py:89-124).
 struct EdgeList {
   std::vector<uint32_t> src, dst, w;
+  uint32_t nparts = 1, rank = 0, shift = 0;
   void reserve(size_t m) { src.reserve(m); dst.reserve(m); w.reserve(m); }
-  void push(uint32_t u, uint32_t v, uint32_t wt) { src.push_back(u); dst.push_back(v); w.push_back(wt); }
+  void push(uint32_t u, uint32_t v, uint32_t wt) {
+    if ((u & (nparts - 1)) != rank || (u == v && wt == 0)) return;
+    src.push_back(u >> shift);
+    dst.push_back(v);
+    w.push_back(wt);
+  }
 };
 
 int check_weights(const mlmq_gen_params_t* p) {
@@ -81,15 +91,15 @@ int sizes(int kind, const mlmq_gen_params_t* p, uint64_t* n, uint64_t* m) {
 
 // Stable counting sort by source; drops (u == v && w == 0).
 uint64_t csr_from_edges(uint64_t n, uint64_t m, const uint32_t* src, const uint32_t* dst,
-                        const uint32_t* w, uint64_t* off, uint32_t* col, uint32_t* wout) {
+                        const uint32_t* w, uint64_t* off, uint32_t* col, uint32_t* wout, bool drop = true) {
   std::memset(off, 0, sizeof(uint64_t) * (n + 1));
   for (uint64_t e = 0; e < m; ++e)
-    if (!(src[e] == dst[e] && w[e] == 0)) off[src[e] + 1]++;
+    if (!(drop && src[e] == dst[e] && w[e] == 0)) off[src[e] + 1]++;
   for (uint64_t i = 0; i < n; ++i) off[i + 1] += off[i];
   std::vector<uint64_t> cursor(off, off + n);
   for (uint64_t e = 0; e < m; ++e) {
     uint32_t u = src[e];
-    if (u == dst[e] && w[e] == 0) continue;
+    if (drop && u == dst[e] && w[e] == 0) continue;
     uint64_t k = cursor[u]++;
     col[k] = dst[e];
     wout[k] = w[e];
@@ -104,8 +114,53 @@ extern "C" int mlmq_gen_size(int kind, const mlmq_gen_params_t* p, uint64_t* n_o
   return sizes(kind, p, n_out, m_out);
 }
 
+static int gen_impl(int kind, const mlmq_gen_params_t* p, const uint32_t* key, uint64_t keylen, uint32_t nparts,
+                    uint32_t rank, uint64_t* off, std::vector<uint32_t>* colv, std::vector<uint32_t>* wv,
+                    uint32_t* col, uint32_t* wout, uint64_t* m_out);
+
 extern "C" int mlmq_gen_graph(int kind, const mlmq_gen_params_t* p, const uint32_t* key,
                               uint64_t keylen, uint64_t* off, uint32_t* col, uint32_t* wout) {
+  uint64_t kept = 0;
+  return gen_impl(kind, p, key, keylen, 1, 0, off, nullptr, nullptr, col, wout, &kept);
+}
+
+// One shard of a generated graph (rows u with u % nparts == rank at local id u / nparts,
+// global columns): the same RNG stream, only the shard's edges are stored.  Two calls:
+// the first (col == NULL) fills off[n_local + 1] and *m_out; the second fills col / w.
+extern "C" int mlmq_gen_shard(int kind, const mlmq_gen_params_t* p, const uint32_t* key, uint64_t keylen,
+                              uint32_t nparts, uint32_t rank, uint64_t* off, uint32_t* col, uint32_t* wout,
+                              uint64_t* m_out) {
+  if (nparts < 1 || (nparts & (nparts - 1)) || rank >= nparts) {
+    mlmq::set_last_error("nparts must be a power of two and rank < nparts");
+    return MLMQ_EINVAL;
+  }
+  if (!m_out) { mlmq::set_last_error("null argument"); return MLMQ_EINVAL; }
+  // generate once, keep the shard's arrays between the sizing and the filling call
+  static thread_local std::vector<uint32_t> s_col, s_w;
+  static thread_local std::vector<uint64_t> s_off;
+  if (!col) {
+    uint64_t n = 0, m = 0;
+    int st = sizes(kind, p, &n, &m);
+    if (st) return st;
+    s_off.assign((n - rank + nparts - 1) / nparts + 1, 0);
+    st = gen_impl(kind, p, key, keylen, nparts, rank, s_off.data(), &s_col, &s_w, nullptr, nullptr, m_out);
+    if (st) return st;
+    if (off) std::memcpy(off, s_off.data(), s_off.size() * sizeof(uint64_t));
+    return MLMQ_OK;
+  }
+  if (*m_out != s_col.size()) { mlmq::set_last_error("mlmq_gen_shard: call it first with col == NULL"); return MLMQ_EINVAL; }
+  std::memcpy(col, s_col.data(), s_col.size() * 4);
+  if (wout) std::memcpy(wout, s_w.data(), s_w.size() * 4);
+  if (off) std::memcpy(off, s_off.data(), s_off.size() * sizeof(uint64_t));
+  std::vector<uint32_t>().swap(s_col);
+  std::vector<uint32_t>().swap(s_w);
+  std::vector<uint64_t>().swap(s_off);
+  return MLMQ_OK;
+}
+
+static int gen_impl(int kind, const mlmq_gen_params_t* p, const uint32_t* key, uint64_t keylen, uint32_t nparts,
+                    uint32_t rank, uint64_t* off, std::vector<uint32_t>* colv, std::vector<uint32_t>* wv,
+                    uint32_t* col, uint32_t* wout, uint64_t* m_out) {
   if (!p || !key || keylen == 0 || !off) { mlmq::set_last_error("null argument"); return MLMQ_EINVAL; }
   uint64_t n = 0, m = 0;
   int st = sizes(kind, p, &n, &m);
@@ -115,7 +170,10 @@ extern "C" int mlmq_gen_graph(int kind, const mlmq_gen_params_t* p, const uint32
     PyRandom rng(key, (size_t)keylen);
     const int64_t wmin = p->wmin, wmax = p->wmax;
     EdgeList E;
-    E.reserve(m);
+    E.nparts = nparts;
+    E.rank = rank;
+    while ((1u << E.shift) < nparts) ++E.shift;
+    E.reserve(nparts > 1 ? m / nparts + m / (4 * nparts) + 1024 : m);
     switch (kind) {
       case MLMQ_GEN_GRID2D: {
         const uint64_t rows = p->rows, cols = p->cols;
@@ -174,8 +232,17 @@ extern "C" int mlmq_gen_graph(int kind, const mlmq_gen_params_t* p, const uint32
         break;
       }
     }
-    uint64_t kept = csr_from_edges(n, E.src.size(), E.src.data(), E.dst.data(), E.w.data(), off, col, wout);
-    if (kept != m) { mlmq::set_last_error("internal: kept %llu of %llu edges", (unsigned long long)kept, (unsigned long long)m); return MLMQ_EINVAL; }
+    const uint64_t n_rows = nparts > 1 ? (n - rank + nparts - 1) / nparts : n;
+    const uint64_t mk = E.src.size();
+    if (colv) {  // shard: caller-owned vectors
+      colv->resize(mk);
+      wv->resize(mk);
+      col = colv->data();
+      wout = wv->data();
+    }
+    uint64_t kept = csr_from_edges(n_rows, mk, E.src.data(), E.dst.data(), E.w.data(), off, col, wout, false);
+    if (nparts == 1 && kept != m) { mlmq::set_last_error("internal: kept %llu of %llu edges", (unsigned long long)kept, (unsigned long long)m); return MLMQ_EINVAL; }
+    *m_out = kept;
   } catch (const std::bad_alloc&) {
     mlmq::set_last_error("host allocation failed while generating %llu edges", (unsigned long long)m);
     return MLMQ_ENOMEM;

@@ -10,6 +10,16 @@ namespace mlmq {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
 
+// Persistent-kernel launch shape: MLMQ_WPB warps per CTA, MLMQ_MINB CTAs per SM
+// (the register budget follows: 65536 / (32 * WPB * MINB) rounded to the allocator).
+#ifndef MLMQ_WPB
+#define MLMQ_WPB 9
+#endif
+#ifndef MLMQ_MINB
+#define MLMQ_MINB 2
+#endif
+constexpr int kWarpsPerBlockMax = MLMQ_WPB;
+
 // Debug hooks (phase profile, wait states, uniformity checks) exist only in the debug
 // library (make debug -> libmlmq_debug.so, loaded when MLMQ_DEBUG=1).
 #ifdef MLMQ_DEBUG_HOOKS

@@ -32,6 +32,9 @@ struct Worker {
 #ifndef MLMQ_PIPE
 #define MLMQ_PIPE 0  // 1: issue step k+1's adjacency loads before step k's checks (2U loads in flight)
 #endif
+#ifndef MLMQ_SEARCH
+#define MLMQ_SEARCH 0  // 1: owner lookup by REDUX over compacted row starts (expand_step_c)
+#endif
 
   const KParams& p;
   S* dist;
@@ -69,6 +72,11 @@ struct Worker {
   bool dist_ovf;
   bool idle;
   int last_src;  // level that served the current batch (1 L0, 2 L1, 3 L2) for diagnostics
+  // bucket floor as last read by this group's bucket_read.  While the group holds work its
+  // unflushed done count keeps the floor from moving, so far_split can bin against it
+  // without another round trip (a stale, lower floor only sends more elements "far",
+  // where bucket_write re-bins them against the current floor).
+  unsigned long long ep_seen;
 
   __device__ Worker(const KParams& prm, unsigned char* sm, int g, int ln) : p(prm), lane(ln), gid(g) {
     L = p.L;
@@ -103,6 +111,7 @@ struct Worker {
     dist_ovf = false;
     pend = ~0ull;
     idle = false;
+    ep_seen = 0;
     __syncwarp();
   }
 
@@ -673,6 +682,7 @@ struct Worker {
     LOC();
     loc(16);
     const unsigned long long e0 = warp_ld(p.ctl + C_EPOCH);
+    ep_seen = e0;
     const int e0mod = (int)(e0 % (unsigned long long)p.bmax);
     bool head_empty = false;
     // managed epochs (bwin > 0): the ring just behind the floor is read first -- it holds
@@ -689,6 +699,7 @@ struct Worker {
           break;
         }
         const unsigned long long en = warp_ld(p.ctl + C_EPOCH);
+        ep_seen = en;
         const int enmod = (int)(en % (unsigned long long)p.bmax);
         const int rel_slot = f >= enmod ? f - enmod : f + p.bmax - enmod;
         int kept = 0;
@@ -1269,7 +1280,7 @@ struct Worker {
   // ============================================================ cascade write
   // compose.py:56-77: L0.write; a full target lane triggers a full transfer of L0 plus
   // the unplaced remainder into L1; L1's write-back goes through to L2.
-  __device__ void cascade_write(const E* src, int k) {
+  __device__ __forceinline__ void cascade_write(const E* src, int k) {
     LOC();
     loc(14);
     const bool has = lane < k;
@@ -1321,7 +1332,7 @@ struct Worker {
     // The floor cannot move while this group holds work (its unflushed done count keeps
     // the near window busy), so far elements are staged across flushes and written as
     // full, bucket-grouped blocks when the stage fills or the group runs out of work.
-    const unsigned long long e = warp_ld(p.ctl + C_EPOCH);
+    const unsigned long long e = ep_seen;
     int kept = 0;
     for (int o = 0; o < outn; o += 32) {
       if (nfar + 32 > p.far_cap) far_flush();
@@ -1346,7 +1357,7 @@ struct Worker {
     outn = kept;
   }
 
-  __device__ void flush_out(bool all) {
+  __device__ __forceinline__ void flush_out(bool all) {
     if (L2K == L2K_BUCKET && p.bwin > 0 && outn > 0) far_split();
     LOC();
     int d = 0;
@@ -1407,7 +1418,12 @@ struct Worker {
     // dequeue-side check (engine.py:190-191) drops.
 #pragma unroll
     for (int j = 0; j < U; ++j)
-      if (act[j]) red_min(dist + v[j], nd[j]);
+      if (act[j]) {
+        red_min(dist + v[j], nd[j]);
+        // v will be expanded soon: warm L2 with its row offsets so the expansion's head
+        // load is an L2 hit (high-diameter graphs pay one such round trip per hop)
+        if (p.adj_prefetch > 1) prefetch_l2(p.off + v[j]);
+      }
     int upd = 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
@@ -1706,6 +1722,42 @@ struct Worker {
     adj_issue(act, kk, a);
   }
 
+  // Owner lookup without the dependent search (MLMQ_SEARCH=1).  The non-empty rows of
+  // the sub-batch are compacted once (lane k holds the k-th non-empty row's start cs, edge
+  // base cb and distance cd); their starts are strictly increasing, so for a window of 32
+  // edge slots one REDUX.OR collects the starts that fall inside it and one REDUX.ADD
+  // counts the rows that began before it: owner(slot) = before + popc(starts <= slot) - 1.
+  // Two warp-wide steps instead of a 5-deep shuffle chain per slot.
+  __device__ __forceinline__ void expand_step_c(int e0, int total, int nne, int cs, unsigned long long cb, S cd,
+                                                bool (&act)[U], S (&dus)[U], uint2 (&a)[U]) {
+    if (e0 >= total) {
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        act[j] = false;
+        dus[j] = 0;
+        a[j] = make_uint2(0u, 0u);
+      }
+      return;
+    }
+    const unsigned lmle = lanemask_lt() | (1u << lane);
+    unsigned long long kk[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int B = e0 + j * 32;
+      const int t = cs - B;
+      const bool mine = lane < nne;
+      const unsigned W = __reduce_or_sync(FULL, (mine && t >= 0 && t < 32) ? (1u << (t & 31)) : 0u);
+      const unsigned before = __reduce_add_sync(FULL, (mine && t < 0) ? 1u : 0u);
+      const int own = (int)(before + __popc(W & lmle)) - 1;
+      const int idx = B + lane;
+      const unsigned long long ob = __shfl_sync(FULL, cb, own & 31);
+      dus[j] = __shfl_sync(FULL, cd, own & 31);
+      act[j] = idx < total;
+      kk[j] = ob + (unsigned long long)idx;
+    }
+    adj_issue(act, kk, a);
+  }
+
   // engine.py:171-227 for one batch in shared memory
   __device__ void relax_batch(int nb) {
     LOC();
@@ -1775,19 +1827,31 @@ struct Worker {
       const int total = __shfl_sync(FULL, incl, 31);
       const int excl = incl - ds;
       const unsigned long long base_e = lo - (unsigned long long)excl;  // edge = base[owner] + slot
+#if MLMQ_SEARCH
+      // compact the non-empty rows once per sub-batch (see expand_step_c)
+      const unsigned nem = __ballot_sync(FULL, ds > 0);
+      const int nne = __popc(nem);
+      const int rk = lane < nne ? (int)__fns(nem, 0, lane + 1) : 0;
+      const int cs = __shfl_sync(FULL, excl, rk);
+      const unsigned long long cb = __shfl_sync(FULL, base_e, rk);
+      const S cd = __shfl_sync(FULL, du, rk);
+#define MLMQ_EXPAND(E0, ACT, DUS, A) expand_step_c(E0, total, nne, cs, cb, cd, ACT, DUS, A)
+#else
+#define MLMQ_EXPAND(E0, ACT, DUS, A) expand_step(E0, total, incl, base_e, du, ACT, DUS, A)
+#endif
 #if MLMQ_PIPE
       // step e0's owner search + adjacency loads are issued one step ahead
       bool act[U];
       S dus[U];
       uint2 a[U];
-      expand_step(0, total, incl, base_e, du, act, dus, a);
+      MLMQ_EXPAND(0, act, dus, a);
       for (int e0 = 0; e0 < total; e0 += 32 * U) {
         LOC();
         const unsigned long long ts0 = pclk();
         bool act2[U];
         S dus2[U];
         uint2 a2[U];
-        expand_step(e0 + 32 * U, total, incl, base_e, du, act2, dus2, a2);
+        MLMQ_EXPAND(e0 + 32 * U, act2, dus2, a2);
         relax_loaded(act, a, dus);
 #pragma unroll
         for (int j = 0; j < U; ++j) {
@@ -1804,11 +1868,12 @@ struct Worker {
         bool act[U];
         S dus[U];
         uint2 a[U];
-        expand_step(e0, total, incl, base_e, du, act, dus, a);
+        MLMQ_EXPAND(e0, act, dus, a);
         relax_loaded(act, a, dus);
         pacc(P_STEPS, ts0);
       }
 #endif
+#undef MLMQ_EXPAND
     }
     const unsigned long long tf0 = pclk();
     flush_out(true);
@@ -2060,10 +2125,7 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
 }
 
 template <int K, int L2K, int CM, int L1T>
-#ifndef MLMQ_MINB
-#define MLMQ_MINB 2
-#endif
-__global__ void __launch_bounds__(288, MLMQ_MINB) mlmq_persistent_kernel(const __grid_constant__ KParams p) {
+__global__ void __launch_bounds__(32 * MLMQ_WPB, MLMQ_MINB) mlmq_persistent_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = blockIdx.x * (blockDim.x >> 5) + warp;

@@ -123,7 +123,6 @@ using namespace mlmq;
 
 namespace {
 
-constexpr int kWarpsPerBlockMax = 9;  // 9 warps per CTA (launch bounds 288 threads)
 constexpr int kOutCap = 32 * 8 + 32;  // L - 1 carried + 32 lanes x U (<= 8) winners
 constexpr int kAuditWords = 14;
 
@@ -600,7 +599,7 @@ KParams make_params(mlmq_graph* g, const mlmq_config_t* c, int dk, const LaunchS
   p.spill_cap = sh.spill_cap;
   p.far_cap = sh.far_cap;
   p.l1_want = std::max(1, std::min(c->read_batch > 0 ? c->read_batch : c->lanes_per_group, sh.batch_cap));
-  p.adj_prefetch = 1;
+  p.adj_prefetch = 1 + ((c->flags & MLMQ_F_PREFETCH_TARGETS) ? 1 : 0);
   p.ring_margin = std::min<long long>((long long)w.bn / 2, 4LL * G + 64);
   p.share = c->share ? 1 : 0;
   p.fifo_park = (sh.l2k == L2K_FIFO && c->fifo_park) ? 1 : 0;
@@ -1199,6 +1198,12 @@ int mlmq_host_alloc(uint64_t bytes, void** out) {
 
 void mlmq_host_free(void* p) {
   if (p) cudaFreeHost(p);
+}
+
+int mlmq_graph_stream(mlmq_graph* g, void** out) {
+  if (!g || !out) { set_last_error("null argument"); return MLMQ_EINVAL; }
+  *out = (void*)g->stream;
+  return MLMQ_OK;
 }
 
 int mlmq_shard_create(const uint64_t* row_offsets, const uint32_t* col, const void* w, int weight_kind,

@@ -52,6 +52,7 @@ class EngineConfig:
                              # reference's floor rule, l2.py:282-287)
     read_batch: int = 64     # elements per L1 read (0 = lanes_per_group, the reference's want)
     hub_threshold: int = 0   # lists longer than this become hub descriptors (0 = 4 x hub_chunk)
+    prefetch_targets: bool = False  # warm L2 with the row offsets of every improved target
     test_capacity: int = 0   # > 0: every queue store gets exactly this many entries (test hook
                              # that forces the QueueOverflowError paths, l2.py:116-135)
 
@@ -193,6 +194,7 @@ def _native_config(cfg: MlmqConfig, eng: EngineConfig, unit_weights: bool,
     c.read_batch = max(0, int(eng.read_batch))
     c.hub_threshold = max(0, int(eng.hub_threshold))
     c.test_capacity = max(0, int(eng.test_capacity))
+    c.flags = (1 if eng.prefetch_targets else 0)
     return c
 
 

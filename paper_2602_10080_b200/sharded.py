@@ -75,21 +75,30 @@ def merge_local(dists: Sequence[np.ndarray], n: int) -> np.ndarray:
 
 
 class GpuShard:
-    """Backend: one shard on one GPU through libmlmq.so."""
+    """Backend: one shard on one GPU through libmlmq.so.
 
-    def __init__(self, graph: CsrGraph, nparts: int, rank: int, config: Optional[MlmqConfig] = None,
+    ``graph`` may be None when ``shard=(row, col, w)`` and ``n_global`` are given (a rank
+    that generated only its own slice, ``_native.generate_shard``); the Δ-type defaults
+    then need ``features`` of the whole graph or explicit config values."""
+
+    def __init__(self, graph: Optional[CsrGraph], nparts: int, rank: int, config: Optional[MlmqConfig] = None,
                  engine: Optional[EngineConfig] = None, *, device: int = 0,
                  watchdog_s: float = DEFAULT_WATCHDOG_S, send_cap: Optional[int] = None,
-                 shard: Optional[Tuple[np.ndarray, np.ndarray, np.ndarray]] = None):
+                 shard: Optional[Tuple[np.ndarray, np.ndarray, np.ndarray]] = None,
+                 n_global: Optional[int] = None, features=None):
         import torch
         self.torch = torch
-        self.nparts, self.rank, self.n_global = nparts, rank, graph.num_vertices
-        cfg, eng = resolve_config(config or MlmqConfig(l2_type="fifo"), engine, graph)
+        if graph is None and (shard is None or n_global is None):
+            raise ValueError("without a graph, pass shard=(row, col, w) and n_global")
+        self.nparts, self.rank = nparts, rank
+        self.n_global = graph.num_vertices if graph is not None else int(n_global)
+        cfg, eng = resolve_config(config or MlmqConfig(l2_type="fifo"), engine, graph, features)
         if cfg.l2_type != "fifo":
             raise ValueError("sharded solves run the FIFO L2 queue")
         row, col, w = shard if shard is not None else shard_csr(graph, nparts, rank)
-        kind = _native.W_F32 if graph.float_weights else _native.W_U32
-        self.dg = _native.DeviceShard(row, col, w, kind, graph.num_vertices, rank, nparts, device)
+        fw = graph.float_weights if graph is not None else np.asarray(w).dtype == np.float32
+        kind = _native.W_F32 if fw else _native.W_U32
+        self.dg = _native.DeviceShard(row, col, w, kind, self.n_global, rank, nparts, device)
         self.m_local = int(col.size)
         ncfg = _native_config(cfg, eng, False, watchdog_s)
         if cfg.num_groups is None:
@@ -103,6 +112,7 @@ class GpuShard:
         self.send = torch.empty(2 * cap, dtype=torch.int32, device=self.device)
         self.send_cap = cap
         self.metrics: List[_native.Metrics] = []
+        self.lib_stream = torch.cuda.ExternalStream(self.dg.stream_ptr(), device=self.device)
 
     def begin(self) -> None:
         self.dg.begin()
@@ -113,8 +123,8 @@ class GpuShard:
         grouped by owner, per-owner counts)."""
         n_in = int(inbox.numel() // 2)
         # the inbox was produced on torch's stream (all-to-all / slicing); the library
-        # runs on its own stream, so order them explicitly
-        self.torch.cuda.current_stream(self.device).synchronize()
+        # runs on its own stream: order them with an event (no host synchronisation)
+        self.lib_stream.wait_stream(self.torch.cuda.current_stream(self.device))
         counts, m = self.dg.step(self.ncfg, inbox.data_ptr() if n_in else 0, n_in,
                                  self.send.data_ptr(), self.send_cap)
         self.metrics.append(m)
@@ -194,15 +204,17 @@ def solve_distributed(backend, source: int, group=None, max_steps: int = 1 << 20
         send, counts = backend.step(inbox)
         steps += 1
         clk.start()
+        # one collective + one host read per superstep: every rank gathers the whole
+        # P x P count matrix, which gives both its receive sizes (its column) and the
+        # global termination test (matrix sum == 0)
         c = torch.tensor(counts, dtype=torch.int64, device=dev)
-        rc = torch.empty_like(c)
-        dist.all_to_all_single(rc, c, group=group)
-        total = c.sum().reshape(1).clone()
-        dist.all_reduce(total, group=group)
-        if int(total.item()) == 0:
+        mat = torch.empty(P * P, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(mat, c, group=group)
+        m = mat.view(P, P).tolist()
+        if sum(map(sum, m)) == 0:
             clk.stop()
             break
-        rcounts = [int(x) for x in rc.tolist()]
+        rcounts = [int(m[src][r]) for src in range(P)]
         recv = torch.empty(2 * sum(rcounts), dtype=torch.int32, device=dev)
         dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=[2 * x for x in rcounts],
                                input_split_sizes=[2 * x for x in counts], group=group)
