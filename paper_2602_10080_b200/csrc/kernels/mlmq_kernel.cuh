@@ -32,6 +32,9 @@ struct Worker {
 #ifndef MLMQ_PIPE
 #define MLMQ_PIPE 0  // 1: issue step k+1's adjacency loads before step k's checks (2U loads in flight)
 #endif
+#ifndef MLMQ_TPF
+#define MLMQ_TPF 0  // 1: split relax step (adjacency issue / loaded check) with the target-offset prefetch
+#endif
 #ifndef MLMQ_SEARCH
 #define MLMQ_SEARCH 0  // 1: owner lookup by REDUX over compacted row starts (expand_step_c)
 #endif
@@ -1442,11 +1445,58 @@ struct Worker {
     __syncwarp();
     if (outn >= L) flush_out(false);
   }
+#if MLMQ_TPF
   __device__ void relax_slots(bool (&act)[U], const unsigned long long (&kk)[U], const S (&du)[U]) {
     uint2 a[U];
     adj_issue(act, kk, a);
     relax_loaded(act, a, du);
   }
+#else
+  // the fused form (loads, checks, RED and compaction in one pass): the lowest register
+  // footprint, used by the default (non-pipelined) expansion
+  __device__ void relax_slots(bool (&act)[U], const unsigned long long (&kk)[U], const S (&du)[U]) {
+    LOC();
+    uint32_t v[U];
+    S nd[U];
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      v[j] = 0;
+      nd[j] = 0;
+      if (act[j]) {
+        const uint2 a = __ldg(p.adj + kk[j]);
+        v[j] = a.x;
+        nd[j] = Tr::add(du[j], p.unit ? 1u : a.y, dist_ovf);
+        ++c;
+        if (nd[j] == (S)Tr::INF) act[j] = false;
+      }
+    }
+    if (p.nparts > 1) relax_remote(act, v, nd);  // 1D-partitioned shard
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (act[j]) act[j] = nd[j] < ldcg_dist(dist + v[j]);
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (act[j]) red_min(dist + v[j], nd[j]);
+    int upd = 0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const unsigned m = __ballot_sync(FULL, act[j]);
+      if (act[j]) {
+        E e;
+        e.v = v[j];
+        e.d = nd[j];
+        outs[outn + __popc(m & lanemask_lt())] = e;
+      }
+      outn += __popc(m);
+      upd += __popc(m);
+    }
+    n_relax += (unsigned)c;  // per lane; folded at exit
+    n_upd += (unsigned)upd;  // warp total, lane-replicated
+    __syncwarp();
+    if (outn >= L) flush_out(false);
+  }
+#endif
 
   // Sharded solve: this group's shard owns global vertices v with
   // v mod P == rank (local id v / P).  Local targets are remapped to local ids and relax
@@ -1528,15 +1578,15 @@ struct Worker {
       }
     }
 #else
+    (void)a;
     for (unsigned long long k0 = lo; k0 < hi; k0 += 32 * U) {
       LOC();
-      adj_issue(act, kk, a);
-      relax_loaded(act, a, dus);
 #pragma unroll
       for (int j = 0; j < U; ++j) {
-        kk[j] += 32 * U;
+        kk[j] = k0 + (unsigned long long)(j * 32 + lane);
         act[j] = kk[j] < hi;
       }
+      relax_slots(act, kk, dus);
     }
 #endif
   }
@@ -1861,7 +1911,7 @@ struct Worker {
         }
         pacc(P_STEPS, ts0);
       }
-#else
+#elif MLMQ_SEARCH
       for (int e0 = 0; e0 < total; e0 += 32 * U) {
         LOC();
         const unsigned long long ts0 = pclk();
@@ -1870,6 +1920,34 @@ struct Worker {
         uint2 a[U];
         MLMQ_EXPAND(e0, act, dus, a);
         relax_loaded(act, a, dus);
+        pacc(P_STEPS, ts0);
+      }
+#else
+      // default: the 5-step shuffle search then the step (loads issued inside the step,
+      // which keeps the register allocation spill-free at 96 registers)
+      for (int e0 = 0; e0 < total; e0 += 32 * U) {
+        LOC();
+        const unsigned long long tq0 = pclk();
+        bool act[U];
+        unsigned long long kk[U];
+        S dus[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const int idx = e0 + j * 32 + lane;
+          int o = 0;
+#pragma unroll
+          for (int s = 16; s >= 1; s >>= 1) {
+            const int probe = __shfl_sync(FULL, incl, o + s - 1);
+            if (probe <= idx) o += s;
+          }
+          const unsigned long long ob = __shfl_sync(FULL, base_e, o);
+          dus[j] = __shfl_sync(FULL, du, o);
+          act[j] = idx < total;
+          kk[j] = ob + (unsigned long long)idx;
+        }
+        pacc(P_SPINS, tq0);
+        const unsigned long long ts0 = pclk();
+        relax_slots(act, kk, dus);
         pacc(P_STEPS, ts0);
       }
 #endif

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -196,6 +197,9 @@ struct mlmq_graph {
   Workspace ws;
   int last_dk = -1;
   bool poisoned = false;  // a kernel did not stop after an abort: the handle is unusable
+  uint32_t* h_stage = nullptr;           // pinned staging of u32 results (copy_dist_u64)
+  unsigned long long stage_cap = 0;
+  cudaEvent_t chunk_ev[8] = {};
   std::mutex mu;
   // sharded solve: 1D partition, v -> shard v mod P, local id v / P
   uint32_t nparts = 1, rank = 0;
@@ -832,18 +836,112 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   return MLMQ_OK;
 }
 
+// Host side of the result copy for 32-bit distances: the u32 array crosses PCIe in
+// kChunks pieces (half the bytes of a u64 copy) and a small persistent pool of host
+// threads widens piece k to u64 (0xFFFFFFFF -> 2^64-1, core.py:17-18) while piece k+1 is
+// still in flight, so the caller's u64 array is ready shortly after the last byte lands.
+constexpr int kChunks = 8;
+struct WidenPool {
+  std::vector<std::thread> th;
+  std::mutex mu;
+  std::condition_variable go, fin;
+  const uint32_t* src = nullptr;
+  uint64_t* dst = nullptr;
+  unsigned long long n = 0, chunk = 0;
+  cudaEvent_t* ev = nullptr;
+  int device = 0, gen = 0, busy = 0;
+  explicit WidenPool(int nt) {
+    for (int t = 0; t < nt; ++t) th.emplace_back([this, t, nt] { loop(t, nt); });
+  }
+  void loop(int t, int nt) {
+    int seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu);
+      go.wait(lk, [&] { return gen != seen; });
+      seen = gen;
+      const uint32_t* s = src;
+      uint64_t* d = dst;
+      const unsigned long long nn = n, ch = chunk;
+      cudaEvent_t* e = ev;
+      const int dev = device;
+      lk.unlock();
+      cudaSetDevice(dev);
+      for (int k = 0; k < kChunks; ++k) {
+        const unsigned long long lo = k * ch, hi = std::min(nn, lo + ch);
+        if (lo >= hi) break;
+        cudaEventSynchronize(e[k]);
+        const unsigned long long part = (hi - lo + nt - 1) / nt;
+        const unsigned long long a = lo + t * part, b = std::min(hi, a + part);
+        for (unsigned long long i = a; i < b; ++i) {
+          const uint32_t x = s[i];
+          d[i] = x == 0xFFFFFFFFu ? ~0ull : (uint64_t)x;
+        }
+      }
+      lk.lock();
+      if (--busy == 0) fin.notify_all();
+    }
+  }
+  std::mutex job_mu;  // one job at a time (graphs may be solved from several host threads)
+  void run(const uint32_t* s, uint64_t* d, unsigned long long nn, unsigned long long ch, cudaEvent_t* e, int dev) {
+    std::lock_guard<std::mutex> job(job_mu);
+    std::unique_lock<std::mutex> lk(mu);
+    src = s, dst = d, n = nn, chunk = ch, ev = e, device = dev;
+    busy = (int)th.size();
+    ++gen;
+    go.notify_all();
+    fin.wait(lk, [&] { return busy == 0; });
+  }
+};
+
+WidenPool& widen_pool() {
+  // detached workers live for the process (never joined: no shutdown-order hazards)
+  static WidenPool* pool = [] {
+    const unsigned hc = std::thread::hardware_concurrency();
+    auto* p = new WidenPool((int)std::max(1u, std::min(8u, hc ? hc : 4u)));
+    for (auto& t : p->th) t.detach();
+    return p;
+  }();
+  return *pool;
+}
+
 int copy_dist_u64(mlmq_graph* g, uint64_t* out) {
   if (g->last_dk < 0) { set_last_error("no solve has run on this graph"); return MLMQ_EINVAL; }
   if (g->last_dk == DK_U64) {
     CK(cudaMemcpyAsync(out, g->d_dist, g->n * 8, cudaMemcpyDeviceToHost, g->stream));
-  } else {
+    CK(cudaStreamSynchronize(g->stream));
+    return MLMQ_OK;
+  }
+  static const bool host_widen = [] {
+    const char* e = getenv("MLMQ_D2H");
+    return !(e && std::strcmp(e, "device") == 0);
+  }();
+  if (g->n < (1ull << 16) || !host_widen) {  // small results (or MLMQ_D2H=device): device widen + one copy
     if (!g->d_dist64) CK(cudaMalloc(&g->d_dist64, std::max<size_t>(8, g->n * 8)));
     const int blocks = (int)std::min<unsigned long long>(8ull * g->sm_count, (g->n + 255) / 256 + 1);
     widen_kernel<<<blocks, 256, 0, g->stream>>>((const uint32_t*)g->d_dist, g->d_dist64, g->n);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, g->d_dist64, g->n * 8, cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    return MLMQ_OK;
   }
-  CK(cudaStreamSynchronize(g->stream));
+  if (g->stage_cap < g->n) {
+    if (g->h_stage) cudaFreeHost(g->h_stage);
+    g->h_stage = nullptr;
+    g->stage_cap = 0;
+    CK(cudaHostAlloc((void**)&g->h_stage, g->n * 4, cudaHostAllocDefault));
+    g->stage_cap = g->n;
+  }
+  if (!g->chunk_ev[0])
+    for (int k = 0; k < kChunks; ++k) CK(cudaEventCreateWithFlags(&g->chunk_ev[k], cudaEventDisableTiming));
+  const unsigned long long ch = (g->n + kChunks - 1) / kChunks;
+  for (int k = 0; k < kChunks; ++k) {
+    const unsigned long long lo = k * ch, hi = std::min(g->n, lo + ch);
+    if (lo < hi)
+      CK(cudaMemcpyAsync(g->h_stage + lo, (const uint32_t*)g->d_dist + lo, (hi - lo) * 4, cudaMemcpyDeviceToHost,
+                         g->stream));
+    CK(cudaEventRecord(g->chunk_ev[k], g->stream));
+  }
+  widen_pool().run(g->h_stage, out, g->n, ch, g->chunk_ev, g->device);
   return MLMQ_OK;
 }
 
@@ -1114,6 +1212,9 @@ void mlmq_graph_destroy(mlmq_graph* g) {
   cudaFree(g->d_seeds);
   cudaFree(g->d_sscratch);
   if (g->h_abort) cudaFreeHost(g->h_abort);
+  if (g->h_stage) cudaFreeHost(g->h_stage);
+  for (cudaEvent_t e : g->chunk_ev)
+    if (e) cudaEventDestroy(e);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->stream) cudaStreamDestroy(g->stream);
