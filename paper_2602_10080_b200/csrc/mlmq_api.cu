@@ -911,11 +911,14 @@ int copy_dist_u64(mlmq_graph* g, uint64_t* out) {
     CK(cudaStreamSynchronize(g->stream));
     return MLMQ_OK;
   }
+  // Default: widen on the device and DMA the u64 array (measured on B200, C2: 0.76 ms of
+  // library overhead vs 0.85 ms for the u32 copy + host-thread widening into the caller's
+  // pinned buffer); MLMQ_D2H=host selects the latter.
   static const bool host_widen = [] {
     const char* e = getenv("MLMQ_D2H");
-    return !(e && std::strcmp(e, "device") == 0);
+    return e && std::strcmp(e, "host") == 0;
   }();
-  if (g->n < (1ull << 16) || !host_widen) {  // small results (or MLMQ_D2H=device): device widen + one copy
+  if (g->n < (1ull << 16) || !host_widen) {  // device widen + one copy
     if (!g->d_dist64) CK(cudaMalloc(&g->d_dist64, std::max<size_t>(8, g->n * 8)));
     const int blocks = (int)std::min<unsigned long long>(8ull * g->sm_count, (g->n + 255) / 256 + 1);
     widen_kernel<<<blocks, 256, 0, g->stream>>>((const uint32_t*)g->d_dist, g->d_dist64, g->n);
