@@ -32,6 +32,9 @@ struct Worker {
 #ifndef MLMQ_PIPE
 #define MLMQ_PIPE 0  // 1: issue step k+1's adjacency loads before step k's checks (2U loads in flight)
 #endif
+#ifndef MLMQ_SHARE_MIN
+#define MLMQ_SHARE_MIN (2 * L)  // eager sharing: local elements a group keeps before giving work away
+#endif
 #ifndef MLMQ_TPF
 #define MLMQ_TPF 0  // 1: split relax step (adjacency issue / loaded check) with the target-offset prefetch
 #endif
@@ -1968,7 +1971,7 @@ struct Worker {
     if (!p.share) return;
     loc(15);
     const int local = l0size + n1 + n2;
-    if (local <= 2 * L) return;
+    if (local <= MLMQ_SHARE_MIN) return;
     unsigned long long idle_now = 0;
     if (lane == 0) idle_now = ld_relaxed(p.ctl + C_IDLE);
     if (__shfl_sync(FULL, idle_now, 0) == 0) return;

@@ -297,14 +297,22 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
     set_last_error("queue configuration needs %lld bytes of shared memory per group; the device allows %d (reduce l1 capacity or block_size)", bytes, max_smem_block);
     return MLMQ_EINVAL;
   }
+  // the kernel's static shared memory (the per-CTA idle-poll cache) comes off the top
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, s->fn));
+  const int dyn_max = max_smem_block - (int)fa.sharedSizeBytes;
+  if (bytes > dyn_max) {
+    set_last_error("queue configuration needs %lld bytes of shared memory per group; the device allows %d (reduce l1 capacity or block_size)", bytes, dyn_max);
+    return MLMQ_EINVAL;
+  }
   s->smem_per_warp = (int)bytes;
-  s->wpb = (int)std::min<long long>(kWarpsPerBlockMax, max_smem_block / bytes);
+  s->wpb = (int)std::min<long long>(kWarpsPerBlockMax, dyn_max / bytes);
   static std::mutex attr_mu;
   static std::unordered_set<const void*> attr_done;
   {
     std::lock_guard<std::mutex> lk(attr_mu);
     if (!attr_done.count(s->fn)) {
-      CK(cudaFuncSetAttribute(s->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_block));
+      CK(cudaFuncSetAttribute(s->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
       attr_done.insert(s->fn);
     }
   }
