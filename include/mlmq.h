@@ -36,7 +36,12 @@ typedef enum {
   MLMQ_EOVERFLOW = 2,  /* QueueOverflowError (l2.py:116-135)                               */
   MLMQ_EENGINE = 3,    /* EngineError: watchdog / audit (engine.py:229-242, 267-279)       */
   MLMQ_ECUDA = 4,      /* EngineError: CUDA runtime failure / no device                    */
-  MLMQ_ENOMEM = 5      /* EngineError: device allocation failed                            */
+  MLMQ_ENOMEM = 5,     /* EngineError: device allocation failed                            */
+  MLMQ_EFORMAT = 6,    /* GraphFormatError (loaders, core.py:49-51)                         */
+  MLMQ_ENEGATIVE = 7,  /* NegativeWeightError (loaders, core.py:53-54)                      */
+  MLMQ_EIO = 8,        /* the file cannot be opened or read (OSError)                       */
+  MLMQ_EFALLBACK = 9   /* input the native loader does not restate exactly (e.g. Python's
+                          "1_000" integer syntax, weights >= 2^32): use the Python reader */
 } mlmq_status;
 
 /* Weight storage kinds accepted by mlmq_graph_create. */
@@ -250,6 +255,19 @@ int mlmq_build_csr(uint64_t n, uint64_t m, const uint32_t* src, const uint32_t* 
  * (splitmix64 of seed ^ edge index; no reference analogue).
  */
 int mlmq_gen_f32_weights(uint64_t m, uint64_t seed, float* w_out);
+
+/*
+ * Native graph readers (graph.py:132-175 load_dimacs, graph.py:185-257 load_matrix_market):
+ * same acceptance rules, messages and edge order, then the build_csr counting sort.
+ *   mlmq_load_*  -> an owned host CSR; mlmq_csr_size / mlmq_csr_copy read it out
+ *   (row_offsets[n+1], col[m], w[m]); mlmq_csr_free releases it.
+ */
+typedef struct mlmq_csr mlmq_csr;
+int mlmq_load_dimacs(const char* path, mlmq_csr** out);
+int mlmq_load_matrix_market(const char* path, int64_t weight_scale, mlmq_csr** out);
+int mlmq_csr_size(const mlmq_csr* c, uint64_t* n, uint64_t* m);
+int mlmq_csr_copy(const mlmq_csr* c, uint64_t* row_offsets, uint32_t* col, uint32_t* w);
+void mlmq_csr_free(mlmq_csr* c);
 
 /*
  * Device queue harness: one L2 queue (l2.py:73-451) in device memory, driven by the same

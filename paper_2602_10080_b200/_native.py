@@ -25,7 +25,8 @@ DEBUG_LIB_PATH = os.path.join(_HERE, "libmlmq_debug.so")
 #: without the per-line trace, so the phase split is representative
 PROF_LIB_PATH = os.path.join(_HERE, "libmlmq_prof.so")
 
-MLMQ_OK, MLMQ_EINVAL, MLMQ_EOVERFLOW, MLMQ_EENGINE, MLMQ_ECUDA, MLMQ_ENOMEM = range(6)
+(MLMQ_OK, MLMQ_EINVAL, MLMQ_EOVERFLOW, MLMQ_EENGINE, MLMQ_ECUDA, MLMQ_ENOMEM, MLMQ_EFORMAT,
+ MLMQ_ENEGATIVE, MLMQ_EIO, MLMQ_EFALLBACK) = range(10)
 W_U32, W_F32, W_UNIT = 0, 1, 2
 DIST_AUTO, DIST_U32, DIST_U64 = 0, 1, 2
 GEN_KINDS = {"grid2d": 0, "path": 1, "uniform": 2, "rmat": 3}
@@ -79,7 +80,8 @@ EXPORTED_SYMBOLS = (
     "mlmq_sssp", "mlmq_sssp_f32", "mlmq_sssp_device", "mlmq_last_dist", "mlmq_reach",
     "mlmq_feature_sums", "mlmq_gen_size", "mlmq_gen_graph", "mlmq_gen_shard", "mlmq_build_csr",
     "mlmq_gen_f32_weights", "mlmq_shard_create", "mlmq_shard_begin", "mlmq_shard_step", "mlmq_graph_stream",
-    "mlmq_host_alloc", "mlmq_host_free", "mlmq_queue_create", "mlmq_queue_destroy",
+    "mlmq_host_alloc", "mlmq_host_free", "mlmq_load_dimacs", "mlmq_load_matrix_market",
+    "mlmq_csr_size", "mlmq_csr_copy", "mlmq_csr_free", "mlmq_queue_create", "mlmq_queue_destroy",
     "mlmq_queue_write", "mlmq_queue_read", "mlmq_queue_stats", "mlmq_queue_stress",
 )
 
@@ -132,6 +134,11 @@ def lib():
             "mlmq_shard_step": ([P, P, P, U64, P, U64, P, P], I32),
             "mlmq_host_alloc": ([U64, P], I32),
             "mlmq_host_free": ([P], None),
+            "mlmq_load_dimacs": ([ctypes.c_char_p, P], I32),
+            "mlmq_load_matrix_market": ([ctypes.c_char_p, ctypes.c_int64, P], I32),
+            "mlmq_csr_size": ([P, P, P], I32),
+            "mlmq_csr_copy": ([P, P, P, P], I32),
+            "mlmq_csr_free": ([P], None),
             "mlmq_queue_create": ([I32, P, P], I32),
             "mlmq_queue_destroy": ([P], None),
             "mlmq_queue_write": ([P, P, U64, ctypes.c_int32], I32),
@@ -387,6 +394,35 @@ def generate(kind: str, seed: int, params: dict):
     key = seed_key(seed)
     check(L.mlmq_gen_graph(GEN_KINDS[kind], ctypes.byref(gp), _ptr(key), key.size,
                            _ptr(off), _ptr(col), _ptr(w)))
+    return off, col, w
+
+
+def load_csr(path: str, fmt: str, weight_scale: int = 1000):
+    """Native DIMACS / Matrix Market reader: (row_offsets u64, col u32, w u32), or None when
+    the file holds input only the Python reader restates exactly (MLMQ_EFALLBACK) or
+    cannot be opened (the Python reader then raises the exact OSError)."""
+    from .core import GraphFormatError, NegativeWeightError
+    L = lib()
+    h = ctypes.c_void_p()
+    bpath = os.fsencode(path)
+    st = (L.mlmq_load_dimacs(bpath, ctypes.byref(h)) if fmt == "dimacs"
+          else L.mlmq_load_matrix_market(bpath, int(weight_scale), ctypes.byref(h)))
+    if st in (MLMQ_EFALLBACK, MLMQ_EIO):
+        return None
+    if st == MLMQ_EFORMAT:
+        raise GraphFormatError(last_error())
+    if st == MLMQ_ENEGATIVE:
+        raise NegativeWeightError(last_error())
+    check(st)
+    try:
+        n, m = ctypes.c_uint64(), ctypes.c_uint64()
+        check(L.mlmq_csr_size(h, ctypes.byref(n), ctypes.byref(m)))
+        off = np.empty(n.value + 1, dtype=np.uint64)
+        col = np.empty(m.value, dtype=np.uint32)
+        w = np.empty(m.value, dtype=np.uint32)
+        check(L.mlmq_csr_copy(h, _ptr(off), _ptr(col), _ptr(w)))
+    finally:
+        L.mlmq_csr_free(h)
     return off, col, w
 
 
