@@ -162,17 +162,25 @@ __global__ void seed_apply_kernel(const uint2* inbox, unsigned long long n_in, S
                                   unsigned long long* err) {
   const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long i = tid; i < n_in; i += stride) {
-    const uint2 m = inbox[i];
-    const unsigned long long lv = (unsigned long long)(m.x >> shift);
-    if (lv >= n_local) {
-      atomicCAS(err, 0ull, (unsigned long long)ERR_CORRUPT);
-      continue;
+  const int lane = threadIdx.x & 31;
+  // whole warps iterate together so the seed append is one fetch-add per warp
+  const unsigned long long n_up = (n_in + 31) & ~31ull;
+  for (unsigned long long i = tid; i < n_up; i += stride) {
+    bool up = false;
+    uint2 m = make_uint2(0u, 0u);
+    unsigned long long lv = 0;
+    if (i < n_in) {
+      m = inbox[i];
+      lv = (unsigned long long)(m.x >> shift);
+      if (lv >= n_local) atomicCAS(err, 0ull, (unsigned long long)ERR_CORRUPT);
+      else up = (S)m.y < atomicMin(dist + lv, (S)m.y);
     }
-    if ((S)m.y < atomicMin(dist + lv, (S)m.y)) {
-      const unsigned long long k = atomicAdd(scratch, 1ull);
-      seeds[k] = make_uint2((uint32_t)lv, m.y);
-    }
+    const unsigned bal = __ballot_sync(FULL, up);
+    if (!bal) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(scratch, (unsigned long long)__popc(bal));
+    base = __shfl_sync(FULL, base, 0);
+    if (up) seeds[base + __popc(bal & lanemask_lt())] = make_uint2((uint32_t)lv, m.y);
   }
 }
 
@@ -222,7 +230,10 @@ __global__ void obox_hist_kernel(const uint2* obox, const unsigned long long* sc
   const unsigned long long n = min(*scratch_n, cap);  // an overflowing step is an error anyway
   const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long i = tid; i < n; i += stride) atomicAdd(h + (obox[i].x & pmask), 1u);
+  for (unsigned long long i = tid; i < n; i += stride) {
+    const uint32_t v = obox[i].x;
+    if (v != 0xFFFFFFFFu) atomicAdd(h + (v & pmask), 1u);  // ~0: an unfilled reserved slot
+  }
   __syncthreads();
   if (threadIdx.x <= pmask && h[threadIdx.x]) atomicAdd(counts + threadIdx.x, (unsigned long long)h[threadIdx.x]);
 }
@@ -233,15 +244,42 @@ __global__ void obox_scan_kernel(const unsigned long long* counts, unsigned long
     s += counts[r];
   }
 }
+// Group the outbox by owner into the send buffer.  Per tile of blockDim x 8 entries a
+// block counts its entries per owner in shared memory, reserves one range per owner with
+// a single global fetch-add, and scatters through shared cursors: 2P global atomics per
+// tile instead of one per entry on P hot cursor words.
 __global__ void obox_scatter_kernel(const uint2* obox, const unsigned long long* scratch_n,
                                     unsigned long long cap, unsigned long long* cursors, uint2* send,
                                     uint32_t pmask) {
+  __shared__ unsigned int cnt[64];
+  __shared__ unsigned long long base[64];
   const unsigned long long n = min(*scratch_n, cap);
-  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long i = tid; i < n; i += stride) {
-    const uint2 m = obox[i];
-    send[atomicAdd(cursors + (m.x & pmask), 1ull)] = m;
+  constexpr int kPer = 8;
+  const unsigned long long tile = (unsigned long long)blockDim.x * kPer;
+  for (unsigned long long t0 = (unsigned long long)blockIdx.x * tile; t0 < n; t0 += (unsigned long long)gridDim.x * tile) {
+    if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    uint2 m[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const unsigned long long i = t0 + (unsigned long long)k * blockDim.x + threadIdx.x;
+      m[k] = i < n ? obox[i] : make_uint2(0xFFFFFFFFu, 0u);
+      if (m[k].x != 0xFFFFFFFFu) atomicAdd(cnt + (m[k].x & pmask), 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x <= pmask) {
+      const unsigned c = cnt[threadIdx.x];
+      base[threadIdx.x] = c ? atomicAdd(cursors + threadIdx.x, (unsigned long long)c) : 0ull;
+      cnt[threadIdx.x] = 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (m[k].x != 0xFFFFFFFFu) {
+        const uint32_t o = m[k].x & pmask;
+        send[base[o] + atomicAdd(cnt + o, 1u)] = m[k];
+      }
+    __syncthreads();
   }
 }
 

@@ -78,6 +78,10 @@ struct Worker {
   bool dist_ovf;
   bool idle;
   int last_src;  // level that served the current batch (1 L0, 2 L1, 3 L2) for diagnostics
+  // sharded solve: this group's private slice of the outbox (reserved kOboxChunk slots at
+  // a time with one fetch-add, so 2663 groups do not serialise on one counter)
+  unsigned long long ob_next;
+  unsigned ob_left;
   // bucket floor as last read by this group's bucket_read.  While the group holds work its
   // unflushed done count keeps the floor from moving, so far_split can bin against it
   // without another round trip (a stale, lower floor only sends more elements "far",
@@ -117,6 +121,8 @@ struct Worker {
     dist_ovf = false;
     pend = ~0ull;
     idle = false;
+    ob_next = 0;
+    ob_left = 0;
     ep_seen = 0;
     __syncwarp();
   }
@@ -1508,6 +1514,15 @@ struct Worker {
   // dropped), and an improving remote relaxation is appended to the outbox as
   // (global v, nd) -- one fetch-add per warp and step -- for the owner to apply after
   // the superstep's exchange.
+  static constexpr unsigned kOboxChunk = 512;
+  // Outbox slots this group reserved but did not fill are marked (v = ~0) so the grouping
+  // kernels skip them.
+  __device__ void obox_close() {
+    for (unsigned k = lane; k < ob_left; k += 32) p.obox[ob_next + k] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+    ob_next += ob_left;
+    ob_left = 0;
+    __syncwarp();
+  }
   __device__ void relax_remote(bool (&act)[U], uint32_t (&v)[U], const S (&nd)[U]) {
     const uint32_t pmask = (uint32_t)p.nparts - 1u;
     S* ghost = reinterpret_cast<S*>(p.ghost);
@@ -1525,26 +1540,37 @@ struct Worker {
         }
       }
     }
+    // the ghost takes a fire-and-forget min (as dist does): an edge that passed the
+    // prefilter is sent even if a racing edge lowers the ghost further; the owner's
+    // inbox apply is a min, so such a duplicate is harmless
 #pragma unroll
     for (int j = 0; j < U; ++j)
-      if (em[j]) em[j] = nd[j] < atomicMin(ghost + v[j], nd[j]);
+      if (em[j]) red_min(ghost + v[j], nd[j]);
 #pragma unroll
     for (int j = 0; j < U; ++j) tot += __popc(__ballot_sync(FULL, em[j]));
     if (tot == 0) return;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(p.obox_n, (unsigned long long)tot);
-    base = __shfl_sync(FULL, base, 0);
-    if (base + (unsigned long long)tot > p.obox_cap) {
-      if (lane == 0) raise_error(ERR_OBOX, base + tot, p.obox_cap, 0, 0);
-      return;
+    if ((unsigned)tot > ob_left) {
+      obox_close();
+      unsigned long long base = 0;
+      const unsigned want = max((unsigned)tot, kOboxChunk);
+      if (lane == 0) base = atomicAdd(p.obox_n, (unsigned long long)want);
+      ob_next = __shfl_sync(FULL, base, 0);
+      ob_left = want;
+      if (ob_next + want > p.obox_cap) {
+        if (lane == 0) raise_error(ERR_OBOX, ob_next + want, p.obox_cap, 0, 0);
+        ob_left = 0;
+        return;
+      }
     }
     int off = 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const unsigned m = __ballot_sync(FULL, em[j]);
-      if (em[j]) p.obox[base + off + __popc(m & lanemask_lt())] = make_uint2(v[j], (uint32_t)nd[j]);
+      if (em[j]) p.obox[ob_next + off + __popc(m & lanemask_lt())] = make_uint2(v[j], (uint32_t)nd[j]);
       off += __popc(m);
     }
+    ob_next += (unsigned long long)tot;
+    ob_left -= (unsigned)tot;
   }
 
   // the whole warp strides one edge list (engine.py:212-220 "big" tier, hub chunks)
@@ -2102,6 +2128,7 @@ struct Worker {
       pacc(P_IDLE, t0);
     }
     pacc(P_TOTAL, tstart);
+    if (p.nparts > 1) obox_close();
     loc(99);
     // exit: metric shard + audit evidence
     if (__any_sync(FULL, dist_ovf) && lane == 0) atomicOr(p.ctl + C_DIST_OVF, 1ull);

@@ -108,7 +108,9 @@ class GpuShard:
         self.device = torch.device("cuda", device)
         # every remote relaxation can improve a ghost at most once per superstep and edge;
         # the kernel reports an overflow instead of writing past the buffer
-        cap = send_cap if send_cap is not None else max(1 << 16, self.m_local + self.dg.n)
+        # (fire-and-forget ghost updates may send an improvement twice when two edges race,
+        # and each group reserves outbox slots 512 at a time: leave room for both)
+        cap = send_cap if send_cap is not None else max(1 << 16, 2 * self.m_local + self.dg.n + (1 << 21))
         self.send = torch.empty(2 * cap, dtype=torch.int32, device=self.device)
         self.send_cap = cap
         self.metrics: List[_native.Metrics] = []
