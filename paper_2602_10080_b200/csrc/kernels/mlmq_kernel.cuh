@@ -38,6 +38,9 @@ struct Worker {
 #ifndef MLMQ_TPF
 #define MLMQ_TPF 0  // 1: split relax step (adjacency issue / loaded check) with the target-offset prefetch
 #endif
+#ifndef MLMQ_HUB_LAST
+#define MLMQ_HUB_LAST 0  // 1: the read cascade tries the L2 queue before hub chunks
+#endif
 #ifndef MLMQ_SEARCH
 #define MLMQ_SEARCH 0  // 1: owner lookup by REDUX over compacted row starts (expand_step_c)
 #endif
@@ -2037,6 +2040,19 @@ struct Worker {
       count(M_L1D, (unsigned long long)c1);
       return c1;
     }
+#if MLMQ_HUB_LAST
+    // hub chunks after the L2 queue: a chunk claimed later re-reads dist[u] and is
+    // skipped when a better copy of u exists, so late hub work is less often wasted
+    t0 = pclk();
+    last_src = 3;
+    const int c2 = l2_read(batch);
+    pacc(P_L2R, t0);
+    if (c2 > 0) return c2;
+    t0 = pclk();
+    const bool h = hub_try();
+    pacc(P_HUB, t0);
+    return h ? -1 : 0;
+#else
     t0 = pclk();
     if (hub_try()) {
       pacc(P_HUB, t0);
@@ -2048,6 +2064,7 @@ struct Worker {
     const int c2 = l2_read(batch);
     pacc(P_L2R, t0);
     return c2;
+#endif
   }
 
   __device__ void run() {
