@@ -402,8 +402,8 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--num-groups", type=_num_groups_arg, help="worker groups while timing (default 1)")
     p.add_argument("--watchdog", type=float, default=60.0)
     p.add_argument("--no-figures", action="store_true")
-    p.add_argument("--timing", choices=("wall", "kernel"), default="wall",
-                   help="record host wall time (reference) or device time (B200 extension)")
+    p.add_argument("--timing", choices=("wall", "kernel"), default="kernel",
+                   help="record device time (default) or host wall time")
     p.add_argument("--device", type=int, default=0)
     p.add_argument("--out", required=True, help="records CSV to write")
     p.set_defaults(fn=cmd_bench)

@@ -38,6 +38,9 @@ struct Worker {
 #ifndef MLMQ_TPF
 #define MLMQ_TPF 0  // 1: split relax step (adjacency issue / loaded check) with the target-offset prefetch
 #endif
+#ifndef MLMQ_SMALLDEG
+#define MLMQ_SMALLDEG 0  // 1: lane-per-row relaxation when every row of a sub-batch has <= U edges
+#endif
 #ifndef MLMQ_HUB_LAST
 #define MLMQ_HUB_LAST 0  // 1: the read cascade tries the L2 queue before hub chunks
 #endif
@@ -1905,6 +1908,25 @@ struct Worker {
       // relaxed edges and the metrics are identical, and on the GPU one load-balanced
       // pass beats a warp-wide walk per list above th_v.
       const int ds = (int)(hi - lo);
+#if MLMQ_SMALLDEG
+      // Short lists (every row of the sub-batch has <= U edges, e.g. road grids): each lane
+      // relaxes its own row directly -- no degree scan, no owner search.  On high-diameter
+      // graphs a group's iteration is a serial chain of warp instructions on the critical
+      // path, so a shorter code path per hop is a shorter solve.
+      if (__reduce_max_sync(FULL, (unsigned)ds) <= (unsigned)U) {
+        bool act[U];
+        unsigned long long kk[U];
+        S dus[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          act[j] = j < ds;
+          kk[j] = lo + (unsigned long long)j;
+          dus[j] = du;
+        }
+        relax_slots(act, kk, dus);
+        continue;
+      }
+#endif
       const int incl = warp_incl_scan(ds, lane);
       const int total = __shfl_sync(FULL, incl, 31);
       const int excl = incl - ds;

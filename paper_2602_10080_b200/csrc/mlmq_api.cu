@@ -733,7 +733,9 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
                        "(create a new one, or restart the process if the device stays busy)");
         return MLMQ_EENGINE;
       }
-      std::this_thread::sleep_for(std::chrono::microseconds(20));
+      // spin for the first 2 ms (short solves return without a sleep quantum of host
+      // latency), then poll every 20 us
+      if (t - t0 > 2e-3) std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
   } else {
     CK(cudaEventSynchronize(g->ev1));
