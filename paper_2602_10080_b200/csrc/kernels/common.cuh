@@ -20,6 +20,18 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 #endif
 constexpr int kWarpsPerBlockMax = MLMQ_WPB;
 
+// MLMQ_ASYNC=1: the flattened expansion stages the next step's adjacency into shared
+// memory with cp.async (LDGSTS) while the current step runs, so two steps of DRAM loads
+// are in flight per lane without holding them in registers.  Per-warp staging: two
+// buffers of 32 x MLMQ_U (col, w) pairs.
+#ifndef MLMQ_ASYNC
+#define MLMQ_ASYNC 0
+#endif
+#ifndef MLMQ_U
+#define MLMQ_U 4
+#endif
+constexpr int kAdjStageBytes = MLMQ_ASYNC ? 2 * 32 * MLMQ_U * 8 + 16 : 0;
+
 // Debug hooks (phase profile, wait states, uniformity checks) exist only in the debug
 // library (make debug -> libmlmq_debug.so, loaded when MLMQ_DEBUG=1).
 #ifdef MLMQ_DEBUG_HOOKS

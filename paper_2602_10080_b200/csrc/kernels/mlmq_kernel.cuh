@@ -25,9 +25,8 @@ struct Worker {
   using Tr = DT<K>;
   using S = typename Tr::S;
   using E = Elem<S>;
-#ifndef MLMQ_U
-#define MLMQ_U 4  // measured on B200 (C2): U=2 2.26 ms, 3 1.69, 4 1.64, 5 1.78, 6 1.88, 8 1.98, 12 2.82
-#endif
+// MLMQ_U (common.cuh, default 4) measured on B200 (C2): U=2 2.26 ms, 3 1.69, 4 1.64, 5 1.78,
+// 6 1.88, 8 1.98, 12 2.82
   static constexpr int U = MLMQ_U;  // edge slots per lane per step (U independent loads in flight)
 #ifndef MLMQ_PIPE
 #define MLMQ_PIPE 0  // 1: issue step k+1's adjacency loads before step k's checks (2U loads in flight)
@@ -1843,6 +1842,39 @@ struct Worker {
     adj_issue(act, kk, a);
   }
 
+  // MLMQ_ASYNC: owner search for step e0, then its adjacency copied into `buf` (this lane's
+  // slots j*32+lane) with cp.async; one commit group per step (empty past the end).
+  __device__ __forceinline__ void stage_step(int e0, int total, int incl, unsigned long long base_e, S du,
+                                             bool (&act)[U], S (&dus)[U], uint2* buf) {
+    if (e0 < total) {
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int idx = e0 + j * 32 + lane;
+        int o = 0;
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          const int probe = __shfl_sync(FULL, incl, o + s - 1);
+          if (probe <= idx) o += s;
+        }
+        const unsigned long long ob = __shfl_sync(FULL, base_e, o);
+        dus[j] = __shfl_sync(FULL, du, o);
+        act[j] = idx < total;
+        if (act[j]) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(buf + j * 32 + lane);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(p.adj + ob + (unsigned long long)idx)
+                       : "memory");
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        act[j] = false;
+        dus[j] = 0;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+
   // engine.py:171-227 for one batch in shared memory
   __device__ void relax_batch(int nb) {
     LOC();
@@ -1964,6 +1996,35 @@ struct Worker {
           a[j] = a2[j];
         }
         pacc(P_STEPS, ts0);
+      }
+#elif MLMQ_ASYNC
+      // adjacency of step k+1 is copied to shared memory (cp.async) while step k runs
+      {
+        uint2* stage = reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(bremap_row + 32) + 15) & ~uintptr_t(15));
+        bool act[U];
+        S dus[U];
+        stage_step(0, total, incl, base_e, du, act, dus, stage);
+        int k = 0;
+        for (int e0 = 0; e0 < total; e0 += 32 * U, ++k) {
+          LOC();
+          const unsigned long long ts0 = pclk();
+          bool act2[U];
+          S dus2[U];
+          stage_step(e0 + 32 * U, total, incl, base_e, du, act2, dus2, stage + ((k + 1) & 1) * (32 * U));
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+          uint2 a[U];
+          const uint2* cur = stage + (k & 1) * (32 * U);
+#pragma unroll
+          for (int j = 0; j < U; ++j) a[j] = act[j] ? cur[j * 32 + lane] : make_uint2(0u, 0u);
+          relax_loaded(act, a, dus);
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            act[j] = act2[j];
+            dus[j] = dus2[j];
+          }
+          pacc(P_STEPS, ts0);
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
 #elif MLMQ_SEARCH
       for (int e0 = 0; e0 < total; e0 += 32 * U) {

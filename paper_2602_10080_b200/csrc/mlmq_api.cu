@@ -289,7 +289,7 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
   s->bscratch = (s->l2k == L2K_BUCKET && c->bmax <= 256) ? 1 : 0;
   s->far_cap = (s->l2k == L2K_BUCKET && c->bucket_window > 0 && c->bmax >= 3) ? kOutCap : 0;
   long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n + s->far_cap) + kMetSlots * 8 +
-                    (s->bscratch ? 20LL * c->bmax : 0LL) + 32LL * 4;
+                    (s->bscratch ? 20LL * c->bmax : 0LL) + 32LL * 4 + kAdjStageBytes;
   bytes = (bytes + 15) / 16 * 16;
   int max_smem_block = 0;
   CK(cudaDeviceGetAttribute(&max_smem_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));

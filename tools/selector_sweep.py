@@ -39,6 +39,12 @@ def corpus():
     g.append(("uniform-1M", generate_graph("uniform", seed=1, n=1 << 20, m=8 << 20, wmin=1, wmax=100)))
     g.append(("path-20k", generate_graph("path", seed=1, n=20000, wmin=1, wmax=9)))
     g.append(("C5-rmat-s24-f32", with_f32_weights(generate_graph("rmat", seed=1, scale=24, edge_factor=16), seed=1)))
+    if os.environ.get("SWEEP_WIDE") == "1":  # round 2: large high-diameter meshes, road-like weights
+        for side in (2048, 3000):
+            g.append((f"grid-{side}", generate_grid2d(side, side, 1, 100, seed=2)))
+            g.append((f"grid-{side}-road", generate_grid2d(side, side, 10, 1000, seed=2)))
+        g.append(("grid-4096x256", generate_grid2d(4096, 256, 1, 100, seed=3)))
+        g.append(("uniform-4M-deg4", generate_graph("uniform", seed=2, n=1 << 22, m=16 << 20, wmin=1, wmax=100)))
     return g
 
 
