@@ -97,11 +97,17 @@ typedef struct {
                                        heap nodes) gets exactly this many entries -- a
                                        test hook that forces the overflow paths (l2.py:116-135) */
   int32_t flags;                    /* MLMQ_F_* engine extensions (0 = none)             */
-  int32_t reserved[2];
+  int32_t heavy_delta;              /* FIFO L2, integer weights: edges with w < heavy_delta
+                                       are relaxed when a vertex is expanded, the rest
+                                       later from a deferred "heavy token" (0 = off)      */
+  float heavy_delta_f;              /* the same threshold for f32 weights (0 = off)       */
 } mlmq_config_t;
 
 /* mlmq_config_t.flags */
 enum { MLMQ_F_PREFETCH_TARGETS = 1 /* prefetch row offsets of improved targets into L2 */ };
+/* bits 8..23 of flags: light/heavy split -- defer the heavy edges of a row only when it has
+ * at least this many of them (smaller rows relax all edges at once) */
+#define MLMQ_F_HEAVY_MIN_SHIFT 8
 
 /*
  * Aggregate counters; the first 11 fields follow core.py:142-154 (METRIC_FIELDS),

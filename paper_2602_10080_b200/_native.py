@@ -50,7 +50,8 @@ class Config(ctypes.Structure):
         ("hub_chunk", ctypes.c_int32), ("share", ctypes.c_int32), ("fifo_park", ctypes.c_int32),
         ("bucket_window", ctypes.c_int32), ("read_batch", ctypes.c_int32),
         ("hub_threshold", ctypes.c_int32), ("test_capacity", ctypes.c_int32),
-        ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
+        ("flags", ctypes.c_int32), ("heavy_delta", ctypes.c_int32),
+        ("heavy_delta_f", ctypes.c_float),
     ]
 
 

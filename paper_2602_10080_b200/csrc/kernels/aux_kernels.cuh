@@ -283,6 +283,38 @@ __global__ void obox_scatter_kernel(const uint2* obox, const unsigned long long*
   }
 }
 
+// Light/heavy row partition for the split relaxation: each row's (col, w) pairs are
+// written to `out` light-first (w < h, compared as u32 bits: valid for integer and for
+// non-negative f32 weights), both classes in their original order, and nlight[u] records
+// the light count.  One warp per row; rows are independent.
+__global__ void partition_rows_kernel(const unsigned long long* off, const uint2* adj, uint2* out,
+                                      uint32_t* nlight, unsigned long long n, uint32_t h) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nw = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+  for (unsigned long long u = w0; u < n; u += nw) {
+    const unsigned long long lo = off[u], hi = off[u + 1];
+    unsigned nl = 0;
+    for (unsigned long long k0 = lo; k0 < hi; k0 += 32) {
+      const unsigned long long k = k0 + lane;
+      nl += __popc(__ballot_sync(FULL, k < hi && adj[k].y < h));
+    }
+    unsigned ls = 0, hs = 0;
+    for (unsigned long long k0 = lo; k0 < hi; k0 += 32) {
+      const unsigned long long k = k0 + lane;
+      const bool has = k < hi;
+      const uint2 x = has ? adj[k] : make_uint2(0u, 0u);
+      const bool light = has && x.y < h;
+      const unsigned lm = __ballot_sync(FULL, light), hm = __ballot_sync(FULL, has && !light);
+      if (light) out[lo + ls + __popc(lm & lanemask_lt())] = x;
+      else if (has) out[lo + nl + hs + __popc(hm & lanemask_lt())] = x;
+      ls += __popc(lm);
+      hs += __popc(hm);
+    }
+    if (lane == 0) nlight[u] = nl;
+  }
+}
+
 // u32 device distances -> u64 API distances (INF -> 2^64-1).
 __global__ void widen_kernel(const uint32_t* in, unsigned long long* out, unsigned long long n) {
   const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;

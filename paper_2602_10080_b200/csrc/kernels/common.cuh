@@ -317,6 +317,12 @@ struct KParams {
   int bwin;                     // bucket window: winners >= bwin buckets above the floor skip L0/L1 (0 = off)
   int batch_cap, out_cap, spill_cap;  // elements
   int far_cap;                  // far staging elements (bucket window), 0 when unused
+  // light/heavy split (FIFO L2, unsharded): rows are partitioned light-first; an expanded
+  // vertex relaxes its light edges at once and defers the heavy ones to a token in ring 1
+  int heavy;                    // 1: split on
+  const uint32_t* nlight;       // [n] light edges at the head of each row
+  int hvy_cap;                  // heavy-token staging elements per group (smem)
+  int heavy_min;                // defer only rows with at least this many heavy edges
   int l1_want;                  // elements per L1 read (reference: lanes_per_group)
   int adj_prefetch;             // prefetch adjacency list heads into L2 at batch start
   long long ring_margin;        // bucket rings: pending blocks kept free for racing writers

@@ -80,6 +80,7 @@ struct Worker {
   int mcursor;
   int outn;
   int nfar;  // far elements staged (bucket window)
+  int nhvy;  // heavy tokens staged (light/heavy split), at fars + far_cap
   bool dist_ovf;
   bool idle;
   int last_src;  // level that served the current batch (1 L0, 2 L1, 3 L2) for diagnostics
@@ -104,7 +105,7 @@ struct Worker {
     l1b = l1a + p.l1cap;
     const int l1n = (L1T == L1K_NEAR_FAR ? 2 : 1) * p.l1cap;
     fars = l1a + l1n;  // far staging (bucket window), p.far_cap elements
-    met = reinterpret_cast<unsigned long long*>(fars + p.far_cap);
+    met = reinterpret_cast<unsigned long long*>(fars + p.far_cap + p.hvy_cap);  // heavy-token stage before it
     met[lane] = 0;  // metric + profile slots (kMetSlots == 32)
     btick = met + kMetSlots;
     bhist = reinterpret_cast<uint32_t*>(btick + (p.bscratch ? p.bmax : 0));
@@ -123,6 +124,7 @@ struct Worker {
     mcursor = p.pnum > 0 ? gid % p.pnum : 0;
     outn = 0;
     nfar = 0;
+    nhvy = 0;
     dist_ovf = false;
     pend = ~0ull;
     idle = false;
@@ -1345,6 +1347,16 @@ struct Worker {
     if (nfar > 0) write_back(fars, 0, nfar, LINEAR);
     nfar = 0;
   }
+  // Light/heavy split: staged heavy tokens (u | kHeavyBit, d) go to the heavy ring (ring 1),
+  // which the read cascade consults only after every other level came up empty.
+  static constexpr uint32_t kHeavyBit = 0x80000000u;
+  __device__ void hvy_flush() {
+    if (nhvy > 0) {
+      count(M_L2E, (unsigned long long)nhvy);
+      ring_write(1, fars + p.far_cap, 0, nhvy, LINEAR);
+    }
+    nhvy = 0;
+  }
   __device__ void far_split() {
     // The floor cannot move while this group holds work (its unflushed done count keeps
     // the near window busy), so far elements are staged across flushes and written as
@@ -1891,8 +1903,13 @@ struct Worker {
       E e = E();
       S du = (S)Tr::INF;
       unsigned long long lo = 0, hi = 0;
+      bool htok = false;  // a deferred heavy-edge token (light/heavy split)
       if (valid) {
         e = batch[i];
+        if (p.heavy) {
+          htok = (e.v & kHeavyBit) != 0;
+          e.v &= ~kHeavyBit;
+        }
         if (e.v >= p.n) {  // never expected: report instead of faulting
           raise_error(ERR_CORRUPT, (unsigned long long)last_src, (unsigned long long)e.v,
                       (unsigned long long)gid, (unsigned long long)i | ((unsigned long long)nb << 32));
@@ -1900,16 +1917,42 @@ struct Worker {
         }
       }
       S cur = (S)Tr::INF;
+      uint32_t nl = 0;
       if (valid) {  // dist[u] and the row offsets are independent loads: issue together
         cur = ldcg_dist(dist + e.v);
         lo = __ldg(p.off + e.v);
         hi = __ldg(p.off + e.v + 1);
+        if (p.heavy) nl = __ldg(p.nlight + e.v);
       }
       if (valid) {
         if (p.dup && e.d > cur) valid = false;  // stale duplicate (engine.py:190-191)
         du = e.d < cur ? e.d : cur;
       }
       if (!valid) lo = hi = 0;
+      if (p.heavy) {
+        // a vertex relaxes its light edges now and leaves a token for the heavy ones; the
+        // token is relaxed later only if no better copy of the vertex appeared meanwhile
+        // (Delta-stepping's light/heavy classification, without bucket synchronisation)
+        // rows with fewer than heavy_min heavy edges relax everything at once: deferring
+        // them would cost a second expansion (head loads, a queue round trip) for little
+        const bool emit = valid && !htok && hi - lo - nl >= (unsigned long long)p.heavy_min && hi > lo + nl;
+        if (valid) {  // (an invalid lane keeps the empty range lo = hi = 0)
+          if (htok) lo += nl;
+          else if (emit) hi = lo + nl;
+        }
+        const unsigned hm = __ballot_sync(FULL, emit);
+        if (hm) {
+          if (nhvy + 32 > p.hvy_cap) hvy_flush();
+          if (emit) {
+            E t;
+            t.v = e.v | kHeavyBit;
+            t.d = du;
+            (fars + p.far_cap)[nhvy + __popc(hm & lanemask_lt())] = t;
+          }
+          nhvy += __popc(hm);
+          __syncwarp();
+        }
+      }
       // warm L2 with the head of each adjacency list while the warp does the scan and
       // the first step's address math (the step's loads then hit L2 instead of DRAM)
       if (valid && p.adj_prefetch) {
@@ -2144,7 +2187,12 @@ struct Worker {
     pacc(P_HUB, t0);
     t0 = pclk();
     last_src = 3;
-    const int c2 = l2_read(batch);
+    int c2 = l2_read(batch);
+    if (L2K == L2K_FIFO && c2 == 0 && p.heavy) {
+      last_src = 4;
+      c2 = ring_read(1, batch);  // deferred heavy-edge tokens, lowest priority
+      if (c2 > 0) count(M_L2D, (unsigned long long)c2);
+    }
     pacc(P_L2R, t0);
     return c2;
 #endif
@@ -2203,6 +2251,10 @@ struct Worker {
         backoff = 0;
         continue;
       }
+      if (L2K == L2K_FIFO && nhvy > 0) {  // staged heavy tokens leave before idling
+        hvy_flush();
+        continue;
+      }
       if (L2K == L2K_BUCKET && nfar > 0) {  // staged far work leaves before idling, and the
         far_flush();                        // cascade runs once more: with bnum > 1 some of
         continue;                           // it may be readable by this very group
@@ -2245,8 +2297,8 @@ struct Worker {
       for (int f = 0; f < M_COUNT; ++f) p.metrics[(size_t)gid * M_COUNT + f] = met[f];
       if (kDebug && p.prof)
         for (int f = 0; f < P_COUNT; ++f) p.prof[(size_t)gid * P_COUNT + f] = met[kProfBase + f];
-      if (l0size + l1size + outn + nfar)
-        atomicAdd(p.ctl + C_LOCAL_NONEMPTY, (unsigned long long)(l0size + l1size + outn + nfar));
+      if (l0size + l1size + outn + nfar + nhvy)
+        atomicAdd(p.ctl + C_LOCAL_NONEMPTY, (unsigned long long)(l0size + l1size + outn + nfar + nhvy));
     }
   }
 };

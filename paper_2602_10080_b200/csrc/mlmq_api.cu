@@ -197,6 +197,9 @@ struct mlmq_graph {
   Workspace ws;
   int last_dk = -1;
   bool poisoned = false;  // a kernel did not stop after an abort: the handle is unusable
+  uint32_t* d_nlight = nullptr;  // light/heavy split: light edges at the head of each row
+  uint32_t part_bits = 0;        // threshold (weight bits) the rows are partitioned by
+  bool part_valid = false;
   uint32_t* h_stage = nullptr;           // pinned staging of u32 results (copy_dist_u64)
   unsigned long long stage_cap = 0;
   cudaEvent_t chunk_ev[8] = {};
@@ -267,10 +270,50 @@ struct LaunchShape {
   const void* fn = nullptr;
   int dk = 0, l2k = 0, cm = 4;
   int smem_per_warp = 0, wpb = 0;
-  int batch_cap = 0, spill_cap = 0, far_cap = 0;
+  int batch_cap = 0, spill_cap = 0, far_cap = 0, hvy_cap = 0;
   int max_groups = 0;
   int bscratch = 0;
 };
+
+// The light/heavy split applies to the FIFO L2 of an unpartitioned graph; returns the
+// threshold as weight bits (0 = off).
+uint32_t heavy_bits(const mlmq_graph* g, const mlmq_config_t* c) {
+  if (c->l2_type != MLMQ_L2_FIFO || g->nparts > 1 || c->unit_weights || g->wkind == MLMQ_W_UNIT) return 0;
+  if (g->wkind == MLMQ_W_F32) {
+    if (!(c->heavy_delta_f > 0.f)) return 0;
+    uint32_t b;
+    std::memcpy(&b, &c->heavy_delta_f, 4);
+    return b;
+  }
+  return c->heavy_delta > 0 ? (uint32_t)c->heavy_delta : 0u;
+}
+
+// Partition every row light-first for threshold bits h (once per threshold; the edge order
+// within a row never changes a distance).
+int ensure_partition(mlmq_graph* g, uint32_t h) {
+  if (g->part_valid && g->part_bits == h) return MLMQ_OK;
+  if (g->n >= 0x80000000ull) { set_last_error("the light/heavy split needs fewer than 2^31 vertices"); return MLMQ_EINVAL; }
+  if (!g->d_nlight) CK(cudaMalloc(&g->d_nlight, std::max<size_t>(4, g->n * 4)));
+  if (g->m) {
+    uint2* tmp = nullptr;
+    cudaError_t e = cudaMalloc(&tmp, g->m * 8);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      set_last_error("light/heavy partition: %s", cudaGetErrorString(e));
+      return MLMQ_ENOMEM;
+    }
+    partition_rows_kernel<<<8 * g->sm_count, 256, 0, g->stream>>>(g->d_off, g->d_adj, tmp, g->d_nlight, g->n, h);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g->stream));
+    cudaFree(g->d_adj);
+    g->d_adj = tmp;
+  } else {
+    CK(cudaMemsetAsync(g->d_nlight, 0, g->n * 4, g->stream));
+  }
+  g->part_bits = h;
+  g->part_valid = true;
+  return MLMQ_OK;
+}
 
 int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) {
   s->dk = dk;
@@ -288,7 +331,8 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
   const int l1n = (c->l1_type == MLMQ_L1_NEAR_FAR ? 2 : 1) * c->l1_capacity;
   s->bscratch = (s->l2k == L2K_BUCKET && c->bmax <= 256) ? 1 : 0;
   s->far_cap = (s->l2k == L2K_BUCKET && c->bucket_window > 0 && c->bmax >= 3) ? kOutCap : 0;
-  long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n + s->far_cap) + kMetSlots * 8 +
+  s->hvy_cap = heavy_bits(g, c) ? 256 : 0;
+  long long bytes = (long long)es * (s->batch_cap + kOutCap + s->spill_cap + l1n + s->far_cap + s->hvy_cap) + kMetSlots * 8 +
                     (s->bscratch ? 20LL * c->bmax : 0LL) + 32LL * 4 + kAdjStageBytes;
   bytes = (bytes + 15) / 16 * 16;
   int max_smem_block = 0;
@@ -340,7 +384,7 @@ int ensure_workspace(mlmq_graph* g, const mlmq_config_t* c, const LaunchShape& s
         std::max<unsigned long long>(65536ull, (4ull * n + 4096ull) * std::min<unsigned long long>(8ull, (32ull + nb - 1) / nb));
     need.hcap = std::max<unsigned long long>(1024ull, 2ull * total / (unsigned long long)need.nheaps);
   } else {
-    need.nrings = sh.l2k == L2K_BUCKET ? c->bmax : 1;
+    need.nrings = sh.l2k == L2K_BUCKET ? c->bmax : (sh.hvy_cap ? 2 : 1);  // ring 1: heavy tokens
     const unsigned long long slots = 8ull * n / (unsigned long long)c->block_size + 16384ull;
     // bucket rings: a quarter of the FIFO ring each (the whole of it with one bucket), and
     // room for every group to race a few blocks into a ring past the occupancy check
@@ -610,6 +654,10 @@ KParams make_params(mlmq_graph* g, const mlmq_config_t* c, int dk, const LaunchS
   p.out_cap = kOutCap;
   p.spill_cap = sh.spill_cap;
   p.far_cap = sh.far_cap;
+  p.heavy = sh.hvy_cap ? 1 : 0;
+  p.hvy_cap = sh.hvy_cap;
+  p.heavy_min = (c->flags >> 8) & 0xFFFF;
+  p.nlight = g->d_nlight;
   p.l1_want = std::max(1, std::min(c->read_batch > 0 ? c->read_batch : c->lanes_per_group, sh.batch_cap));
   p.adj_prefetch = 1 + ((c->flags & MLMQ_F_PREFETCH_TARGETS) ? 1 : 0);
   p.ring_margin = std::min<long long>((long long)w.bn / 2, 4LL * G + 64);
@@ -642,6 +690,7 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
     return MLMQ_EINVAL;
   }
   const unsigned long long hub_chunk = c->hub_chunk > 0 ? std::min<unsigned long long>((unsigned long long)c->hub_chunk, 1ull << 20) : 2048ull;
+  if (sh.hvy_cap && (st = ensure_partition(g, heavy_bits(g, c)))) return st;
   if ((st = ensure_workspace(g, c, sh, hub_chunk, G))) return st;
   if (g->metrics_cap < (unsigned long long)G) {
     cudaFree(g->d_metrics);
@@ -1224,6 +1273,7 @@ void mlmq_graph_destroy(mlmq_graph* g) {
   cudaFree(g->d_obox);
   cudaFree(g->d_seeds);
   cudaFree(g->d_sscratch);
+  cudaFree(g->d_nlight);
   if (g->h_abort) cudaFreeHost(g->h_abort);
   if (g->h_stage) cudaFreeHost(g->h_stage);
   for (cudaEvent_t e : g->chunk_ev)

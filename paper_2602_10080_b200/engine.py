@@ -53,6 +53,10 @@ class EngineConfig:
     read_batch: int = 64     # elements per L1 read (0 = lanes_per_group, the reference's want)
     hub_threshold: int = 0   # lists longer than this become hub descriptors (0 = 4 x hub_chunk)
     prefetch_targets: bool = False  # warm L2 with the row offsets of every improved target
+    heavy_delta: float = 0.0  # FIFO L2: edges with w < heavy_delta are relaxed when a vertex is
+                              # expanded, heavier ones later from a deferred token (0 = off)
+    heavy_min_edges: int = 0  # defer only rows with at least this many heavy edges (0: every row;
+                              # measured best on C2/C5: larger values re-expand the small rows)
     test_capacity: int = 0   # > 0: every queue store gets exactly this many entries (test hook
                              # that forces the QueueOverflowError paths, l2.py:116-135)
 
@@ -194,7 +198,10 @@ def _native_config(cfg: MlmqConfig, eng: EngineConfig, unit_weights: bool,
     c.read_batch = max(0, int(eng.read_batch))
     c.hub_threshold = max(0, int(eng.hub_threshold))
     c.test_capacity = max(0, int(eng.test_capacity))
-    c.flags = (1 if eng.prefetch_targets else 0)
+    c.flags = (1 if eng.prefetch_targets else 0) | (max(0, min(0xFFFF, int(eng.heavy_min_edges))) << 8)
+    hd = float(eng.heavy_delta or 0.0)
+    c.heavy_delta = int(round(hd)) if hd >= 1 else 0
+    c.heavy_delta_f = hd if hd > 0 else 0.0
     return c
 
 

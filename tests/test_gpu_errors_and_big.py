@@ -117,8 +117,11 @@ def c4_graph():
 
 def test_c4_kronecker_s26_matches_golden_hash(c4_graph):
     # BASELINE.json configs[3] on one B200 (the whole 1.07 B-edge graph fits in HBM)
-    from bench import solve_config
+    from bench import solve_config, solve_engine
     f = extract_features(c4_graph)
+    r = sssp_solve(c4_graph, 0, solve_config("c4", c4_graph, f), solve_engine("c4"), features=f)
+    assert oracle.dist_sha256(r.dist_array) == BIG["c4"]["dist_sha256"]
+    assert r.metrics.relaxations < 1.2 * BIG["c4"]["e_reach"]  # light/heavy split at work
     r = sssp_solve(c4_graph, 0, solve_config("c4", c4_graph, f), EngineConfig(bucket_window=1), features=f)
     assert oracle.dist_sha256(r.dist_array) == BIG["c4"]["dist_sha256"]
     m = r.metrics
@@ -143,9 +146,10 @@ def test_c2_sharded_matches_reference_hash():
 
 
 def test_c5_float_weights_match_golden_hash():
-    from bench import build_graph, solve_config
+    from bench import build_graph, solve_config, solve_engine
     g = build_graph("c5")
     f = extract_features(g)
-    r = sssp_solve(g, 0, solve_config("c5", g, f), features=f)
-    d = np.ascontiguousarray(r.dist_array, dtype="<f4")
-    assert hashlib.sha256(d.tobytes()).hexdigest() == BIG["c5"]["dist_f32_sha256"]
+    for eng in (EngineConfig(), solve_engine("c5")):  # without and with the light/heavy split
+        r = sssp_solve(g, 0, solve_config("c5", g, f), eng, features=f)
+        d = np.ascontiguousarray(r.dist_array, dtype="<f4")
+        assert hashlib.sha256(d.tobytes()).hexdigest() == BIG["c5"]["dist_f32_sha256"]

@@ -285,7 +285,8 @@ def test_random_sources_and_configs_fuzz():
             lanes_per_group=rng.choice([1, 2, 5, 8, 32]),
             th_v=rng.choice([0, 16, 100000]))
         s = rng.randrange(g.num_vertices)
-        r = sssp_solve(g, s, cfg, EngineConfig(duplicate_elimination=rng.random() < 0.8),
+        r = sssp_solve(g, s, cfg, EngineConfig(duplicate_elimination=rng.random() < 0.8,
+                                               heavy_delta=rng.choice([0, 0, 4, 64])),
                        watchdog_s=30)
         want = oracle_dist(g, s)
         assert compare_distances(r.dist_array, want) is None, (trial, cfg)
@@ -333,13 +334,34 @@ C3_DIST = "2bf8e0cf2ab0c6ab8b906952288c22c564fbda5404ab78d48e8c90590c3bde41"
 def test_baseline_configs_match_reference_hashes(name, sha):
     # the bench's own engine configurations on the BASELINE graphs, against the
     # reference dijkstra_oracle's dist_sha256 (produced by the reference)
-    from bench import build_graph, solve_config
+    from bench import build_graph, solve_config, solve_engine
     g = build_graph(name)
     f = extract_features(g)
     for _ in range(2):
-        r = sssp_solve(g, 0, solve_config(name, g, f), EngineConfig(bucket_window=1), features=f)
+        r = sssp_solve(g, 0, solve_config(name, g, f), solve_engine(name), features=f)
         assert oracle.dist_sha256(r.dist_array) == sha
         assert_balanced(r.metrics)
+
+
+@pytest.mark.parametrize("heavy,hmin", [(8, 0), (24, 0), (128, 0), (24, 16)])
+def test_light_heavy_split_exact(heavy, hmin):
+    # FIFO L2 with the light/heavy split (B200 extension): exact on every graph family,
+    # group count and L1 variant; the deferred tokens leave no residue (counter identities)
+    graphs = [generate_graph("rmat", seed=7, scale=12, edge_factor=16, wmin=1, wmax=255),
+              generate_grid2d(40, 40, 1, 100, seed=4),
+              generate_graph("path", seed=1, n=500, wmin=1, wmax=30),
+              generate_random_uniform(3000, 20000, 1, 200, seed=2)]
+    for g in graphs:
+        want = oracle_dist(g)
+        for l1 in ("vector", "near_far", "filter", "slf"):
+            for groups in (1, 7, None):
+                cfg = MlmqConfig(l1_type=l1, l2_type="fifo", num_groups=groups)
+                r = sssp_solve(g, 0, cfg, EngineConfig(heavy_delta=heavy, heavy_min_edges=hmin))
+                assert np.array_equal(r.dist_array, want), (l1, groups, g.num_vertices)
+                assert_balanced(r.metrics)
+    gf = with_f32_weights(generate_graph("rmat", seed=1, scale=12, edge_factor=16), seed=3)
+    r = sssp_solve(gf, 0, MlmqConfig(num_groups=None), EngineConfig(heavy_delta=0.05))
+    assert np.array_equal(r.dist_array, oracle.dijkstra_f32(gf.row_offsets, gf.col_indices, gf.weights, 0))
 
 
 def test_recycled_result_buffers_are_not_aliased():

@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np  # noqa: E402
 
-from bench import build_graph, solve_config  # noqa: E402
+from bench import build_graph, solve_config, solve_engine  # noqa: E402
 from paper_2602_10080_b200 import EngineConfig, extract_features  # noqa: E402
 from paper_2602_10080_b200.engine import prepare  # noqa: E402
 
@@ -46,7 +46,7 @@ def main():
     print(f"graph {a.config} n={g.num_vertices} m={g.num_edges} gen {time.perf_counter() - t:.1f}s", flush=True)
     f = extract_features(g)
     cfg = solve_config(a.config, g, f)
-    eng = EngineConfig(bucket_window=1)
+    eng = solve_engine(a.config)
     for kv in a.set:
         k, v = kv.split("=", 1)
         v = _num(v)
