@@ -205,6 +205,27 @@ __device__ __forceinline__ Elem<unsigned long long> ld_cg_elem(const Elem<unsign
   e.d = ((unsigned long long)r.w << 32) | r.z;
   return e;
 }
+// Adjacency (col, w) load.  MLMQ_ADJ_HINT: 0 read-only path (__ldg), 1 cache-streaming
+// (__ldcs), 2 (default) L1 no-allocate + L2 evict-first policy, so the streamed adjacency
+// does not push the distance array and row offsets out of L2 (B200: C2 1.42 -> 1.41 ms,
+// C4 20.8 -> 20.3 ms, C5 7.01 -> 6.85 ms; profiles/r2_experiments.md).
+#ifndef MLMQ_ADJ_HINT
+#define MLMQ_ADJ_HINT 2
+#endif
+__device__ __forceinline__ uint2 ld_adj(const uint2* p) {
+#if MLMQ_ADJ_HINT == 1
+  return __ldcs(p);
+#elif MLMQ_ADJ_HINT == 2
+  uint2 r;
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+      : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
+  return r;
+#else
+  return __ldg(p);
+#endif
+}
 __device__ __forceinline__ uint32_t ldcg_dist(const uint32_t* p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned long long ldcg_dist(const unsigned long long* p) { return __ldcg(p); }
 

@@ -37,6 +37,9 @@ struct Worker {
 #ifndef MLMQ_TPF
 #define MLMQ_TPF 0  // 1: split relax step (adjacency issue / loaded check) with the target-offset prefetch
 #endif
+#ifndef MLMQ_DIRECT_TOKEN
+#define MLMQ_DIRECT_TOKEN 0  // 1: improved targets without light edges become heavy tokens at once
+#endif
 #ifndef MLMQ_SMALLDEG
 #define MLMQ_SMALLDEG 0  // 1: lane-per-row relaxation when every row of a sub-batch has <= U edges
 #endif
@@ -1418,7 +1421,7 @@ struct Worker {
   // (relax_loaded), so a warp keeps 2U independent DRAM loads in flight per lane.
   __device__ __forceinline__ void adj_issue(const bool (&act)[U], const unsigned long long (&kk)[U], uint2 (&a)[U]) const {
 #pragma unroll
-    for (int j = 0; j < U; ++j) a[j] = act[j] ? __ldg(p.adj + kk[j]) : make_uint2(0u, 0u);
+    for (int j = 0; j < U; ++j) a[j] = act[j] ? ld_adj(p.adj + kk[j]) : make_uint2(0u, 0u);
   }
   __device__ void relax_loaded(bool (&act)[U], const uint2 (&a)[U], const S (&du)[U]) {
     LOC();
@@ -1490,7 +1493,7 @@ struct Worker {
       v[j] = 0;
       nd[j] = 0;
       if (act[j]) {
-        const uint2 a = __ldg(p.adj + kk[j]);
+        const uint2 a = ld_adj(p.adj + kk[j]);
         v[j] = a.x;
         nd[j] = Tr::add(du[j], p.unit ? 1u : a.y, dist_ovf);
         ++c;
@@ -1498,6 +1501,17 @@ struct Worker {
       }
     }
     if (p.nparts > 1) relax_remote(act, v, nd);  // 1D-partitioned shard
+#if MLMQ_DIRECT_TOKEN
+    // light/heavy split: the light-edge count of each target is loaded beside the
+    // prefilter; an improved target without light edges needs no light pass, so it goes
+    // straight to the heavy ring as a token (one queue hop and one expansion fewer)
+    unsigned nz = 0;  // bit j: target j has no light edges
+    if (p.heavy) {
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+        if (act[j] && __ldg(p.nlight + v[j]) == 0u) nz |= 1u << j;
+    }
+#endif
 #pragma unroll
     for (int j = 0; j < U; ++j)
       if (act[j]) act[j] = nd[j] < ldcg_dist(dist + v[j]);
@@ -1507,8 +1521,26 @@ struct Worker {
     int upd = 0;
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const unsigned m = __ballot_sync(FULL, act[j]);
-      if (act[j]) {
+#if MLMQ_DIRECT_TOKEN
+      const bool tok = act[j] && ((nz >> j) & 1u);
+      const bool nrm = act[j] && !tok;
+      const unsigned tm = __ballot_sync(FULL, tok);
+      if (tm) {
+        if (nhvy + 32 > p.hvy_cap) hvy_flush();
+        if (tok) {
+          E t;
+          t.v = v[j] | kHeavyBit;
+          t.d = nd[j];
+          (fars + p.far_cap)[nhvy + __popc(tm & lanemask_lt())] = t;
+        }
+        nhvy += __popc(tm);
+        upd += __popc(tm);
+      }
+#else
+      const bool nrm = act[j];
+#endif
+      const unsigned m = __ballot_sync(FULL, nrm);
+      if (nrm) {
         E e;
         e.v = v[j];
         e.d = nd[j];

@@ -200,6 +200,7 @@ struct mlmq_graph {
   uint32_t* d_nlight = nullptr;  // light/heavy split: light edges at the head of each row
   uint32_t part_bits = 0;        // threshold (weight bits) the rows are partitioned by
   bool part_valid = false;
+  bool l2win_set = false, l2win_failed = false;  // apply_l2_window state
   uint32_t* h_stage = nullptr;           // pinned staging of u32 results (copy_dist_u64)
   unsigned long long stage_cap = 0;
   cudaEvent_t chunk_ev[8] = {};
@@ -484,6 +485,50 @@ bool debug_enabled() {
   return v == 1;
 }
 
+// The distance array as a persisting L2 access-policy window on the library stream: the
+// K1 prefilter loads of dist[v] are random and compete for L2 with the streamed adjacency.
+// Default: only when the whole array fits the persisting carve-out (B200: 79 MB; C5's
+// 67 MB: 6.85 -> 6.65 ms, C2 neutral; a partial window on C4's 268 MB costs 16 %).
+// MLMQ_L2PERSIST=<fraction> forces a window of that fraction, 0 turns it off.
+void apply_l2_window(mlmq_graph* g, int dk) {
+  static const float frac = [] {
+    const char* e = getenv("MLMQ_L2PERSIST");
+    return e ? (float)atof(e) : -1.f;
+  }();
+  if (frac == 0.f || g->l2win_failed) return;
+  int maxp = 0, maxw = 0;
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
+  cudaGetLastError();
+  const size_t bytes = (size_t)g->n * (dk == DK_U64 ? 8 : 4);
+  if (maxp <= 0 || maxw <= 0 || (frac < 0.f && (bytes > (size_t)maxp || bytes > (size_t)maxw))) {
+    if (g->l2win_set) {  // a different distance kind no longer fits: drop the window
+      cudaStreamAttrValue a = {};
+      cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &a);
+      g->l2win_set = false;
+    }
+    cudaGetLastError();
+    return;
+  }
+  const double f = frac < 0.f ? 1.0 : (double)frac;
+  const size_t win = std::min(bytes, (size_t)maxw);
+  const size_t lim = std::min((size_t)maxp, (size_t)(win * f));
+  size_t cur = 0;
+  if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) != cudaSuccess || cur < lim)
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+  cudaStreamAttrValue a = {};
+  a.accessPolicyWindow.base_ptr = g->d_dist;
+  a.accessPolicyWindow.num_bytes = win;
+  a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)lim / (double)win);
+  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  if (cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &a) != cudaSuccess)
+    g->l2win_failed = true;  // best effort: never fail a solve over a cache hint
+  else
+    g->l2win_set = true;
+  cudaGetLastError();
+}
+
 // MLMQ_DEBUG=1: per-phase cycle breakdown and the wait states of stuck warps.
 void debug_dump(mlmq_graph* g, int G, const char* tag) {
   std::vector<unsigned long long> pr((size_t)G * P_COUNT), ws((size_t)2 * G + 8 + (size_t)G * 32 + 8192);
@@ -741,6 +786,7 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
       CK(cudaGetLastError());
     }
   }
+  apply_l2_window(g, dk);
   void* args[] = {(void*)&p};
   CK(cudaLaunchCooperativeKernel(sh.fn, dim3(blocks), dim3(sh.wpb * 32), args,
                                  (size_t)sh.wpb * sh.smem_per_warp, g->stream));

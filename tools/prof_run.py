@@ -70,8 +70,11 @@ def main():
           f"{cfg_r.l1_type}+{cfg_r.l2_type} delta={cfg_r.l2_params.delta}", flush=True)
     if a.check:
         from oracle import oracle
-        want = oracle.dijkstra_u64(g.row_offsets, g.col_indices, g.weights, a.source)
         got = dg.last_dist()
+        if np.asarray(g.weights).dtype.kind == "f":
+            want = oracle.dijkstra_f32(g.row_offsets, g.col_indices, g.weights, a.source)
+        else:
+            want = oracle.dijkstra_u64(g.row_offsets, g.col_indices, g.weights, a.source)
         print("oracle match:", bool(np.array_equal(got, want)), flush=True)
 
 
