@@ -2402,6 +2402,16 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
       }
     } else {
       kq = 0;
+      if ((kDebug && p.wstate) && lane == 0 && p.bwin == 0 && (it & 3) == 0) {
+        // timeline (debug/profile builds): (time, busy groups, outstanding units) every
+        // 4th poll, so the parallelism profile of a FIFO solve can be read back
+        unsigned long long* E = p.wstate + 2 * (size_t)p.G + 8 + (size_t)p.G * 32;
+        const unsigned long long i = ++E[0];
+        const unsigned long long busy = (unsigned long long)p.G - ld_relaxed(p.ctl + C_IDLE);
+        const unsigned long long out = r > d ? r - d : 0ull;
+        if (i < 8192)
+          E[i] = ((globaltimer_ns() >> 6) << 40) | ((busy & 0xFFFF) << 24) | (out > 0xFFFFFFull ? 0xFFFFFFull : out);
+      }
     }
     if ((kDebug && p.wstate) && lane == 0) {
       p.wstate[2 * (size_t)p.G] += 1;

@@ -597,10 +597,29 @@ void debug_dump(mlmq_graph* g, int G, const char* tag) {
       }
     }
   }
-  {  // managed-floor epoch log: [0] count, then (timestamp << 16 | busy groups) per advance
+  {  // managed-floor epoch log: [0] count, then (timestamp << 16 | busy groups) per advance;
+     // without a managed floor: the timeline ((t >> 6) << 40 | busy << 24 | outstanding)
     const unsigned long long* E = &ws[(size_t)2 * G + 8 + (size_t)G * 32];
     const unsigned long long ne = std::min<unsigned long long>(E[0], 8191);
-    if (ne > 1) {
+    if (ne > 1 && ctl[C_EPOCH] == 0) {
+      const double t0 = (double)(E[1] >> 40) * 64.0, t1 = (double)(E[ne] >> 40) * 64.0;
+      const int NB = 24;
+      double sb[NB] = {0}, so[NB] = {0};
+      int cnt[NB] = {0};
+      for (unsigned long long i = 1; i <= ne; ++i) {
+        const double t = (double)(E[i] >> 40) * 64.0;
+        int b = t1 > t0 ? (int)((t - t0) / (t1 - t0) * NB) : 0;
+        b = std::min(NB - 1, std::max(0, b));
+        sb[b] += (double)((E[i] >> 24) & 0xFFFF);
+        so[b] += (double)(E[i] & 0xFFFFFF);
+        cnt[b]++;
+      }
+      fprintf(stderr, "[mlmq debug]   timeline %.1f us, %llu samples (bin: busy groups / outstanding units):", (t1 - t0) / 1e3, ne);
+      for (int b = 0; b < NB; ++b)
+        if (cnt[b]) fprintf(stderr, " %.0f/%.0f", sb[b] / cnt[b], so[b] / cnt[b]);
+        else fprintf(stderr, " -");
+      fprintf(stderr, "\n");
+    } else if (ne > 1) {
       std::vector<double> d;
       double busy = 0;
       for (unsigned long long i = 2; i <= ne; ++i) {
