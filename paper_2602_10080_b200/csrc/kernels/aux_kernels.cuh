@@ -315,13 +315,94 @@ __global__ void partition_rows_kernel(const unsigned long long* off, const uint2
   }
 }
 
-// u32 device distances -> u64 API distances (INF -> 2^64-1).
-__global__ void widen_kernel(const uint32_t* in, unsigned long long* out, unsigned long long n) {
+// u32 device distances -> u64 API distances (INF -> 2^64-1), in caller vertex order
+// (perm = caller id -> device id of a relabeled graph, or null).
+__global__ void widen_kernel(const uint32_t* in, unsigned long long* out, unsigned long long n,
+                             const uint32_t* perm) {
   const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   for (unsigned long long i = tid; i < n; i += stride) {
-    const uint32_t v = in[i];
+    const uint32_t v = in[perm ? __ldg(perm + i) : i];
     out[i] = v == 0xFFFFFFFFu ? ~0ull : (unsigned long long)v;
+  }
+}
+
+// out[i] = in[perm[i]]: device-order distances back to caller order (4- or 8-byte words).
+template <class T>
+__global__ void gather_kernel(const T* in, T* out, unsigned long long n, const uint32_t* perm) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n; i += stride) out[i] = in[__ldg(perm + i)];
+}
+
+// ---- vertex relabeling by in-degree class (B200 layout; see ensure_relabel) ----
+// indeg[v] += 1 per edge targeting v; warp-aggregated when a warp's lanes share a target
+// (the hubs of a power-law graph take most of the edges).
+__global__ void indeg_kernel(const uint2* adj, unsigned long long m, uint32_t* indeg) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (unsigned long long k0 = tid - lane; k0 < m; k0 += stride) {
+    const unsigned long long k = k0 + lane;
+    const bool has = k < m;
+    const uint32_t v = has ? adj[k].x : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(FULL, v);
+    if (has && (__ffs(peers) - 1) == lane) atomicAdd(indeg + v, (uint32_t)__popc(peers));
+  }
+}
+
+// key[v] = in-degree class, hottest first: 4 classes per octave of in-degree, vertices that
+// no edge reaches last; val[v] = v.  Also max in-degree into *mx.
+__global__ void relabel_keys_kernel(const uint32_t* indeg, unsigned long long n, uint8_t* key, uint32_t* val,
+                                    unsigned int* mx) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned int m = 0;
+  for (unsigned long long i = tid; i < n; i += stride) {
+    const uint32_t d = indeg[i];
+    m = d > m ? d : m;
+    int k = 255;
+    if (d > 0) {
+      const int lg = 31 - __clz(d);                                   // octave
+      const int sub = lg >= 2 ? (int)((d >> (lg - 2)) & 3u) : (int)(d & ((1u << lg) - 1u)) << (2 - lg);
+      k = 254 - (lg * 4 + sub);                                       // 2^31 -> 130, 1 -> 254
+    }
+    key[i] = (uint8_t)k;
+    val[i] = (uint32_t)i;
+  }
+  m = __reduce_max_sync(FULL, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
+// perm[iperm[i]] = i; ndeg[i] = degree of the vertex that becomes row i.
+__global__ void relabel_perm_kernel(const uint32_t* iperm, const unsigned long long* off, unsigned long long n,
+                                    uint32_t* perm, unsigned long long* ndeg) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n; i += stride) {
+    const uint32_t u = iperm[i];
+    perm[u] = (uint32_t)i;
+    ndeg[i] = off[u + 1] - off[u];
+  }
+  if (tid == 0) ndeg[n] = 0;
+}
+
+// Row i of the relabeled CSR = row iperm[i] of the old one, targets renamed through perm,
+// edge order kept.  One warp per row.
+__global__ void relabel_rows_kernel(const unsigned long long* off, const uint2* adj, const uint32_t* iperm,
+                                    const uint32_t* perm, const unsigned long long* noff, uint2* nadj,
+                                    unsigned long long n) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long w0 = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nw = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+  for (unsigned long long i = w0; i < n; i += nw) {
+    const uint32_t u = iperm[i];
+    const unsigned long long lo = off[u], hi = off[u + 1], o = noff[i];
+    for (unsigned long long k = lo + lane; k < hi; k += 32) {
+      uint2 x = adj[k];
+      x.x = __ldg(perm + x.x);
+      nadj[o + (k - lo)] = x;
+    }
   }
 }
 

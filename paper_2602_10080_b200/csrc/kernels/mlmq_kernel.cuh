@@ -2427,7 +2427,11 @@ static __device__ __noinline__ void manager_loop(const KParams& p, int lane) {
 }
 
 template <int K, int L2K, int CM, int L1T>
+#ifdef MLMQ_MAXNREG  // experiment: an explicit register cap instead of the min-blocks bound
+__global__ void __maxnreg__(MLMQ_MAXNREG) mlmq_persistent_kernel(const __grid_constant__ KParams p) {
+#else
 __global__ void __launch_bounds__(32 * MLMQ_WPB, MLMQ_MINB) mlmq_persistent_kernel(const __grid_constant__ KParams p) {
+#endif
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = blockIdx.x * (blockDim.x >> 5) + warp;
