@@ -20,6 +20,98 @@
 
 namespace mlmq {
 
+#ifndef MLMQ_COLD_RING
+#define MLMQ_COLD_RING 1
+#endif
+
+// The L2 block-ring writer (l2.py:96-114) as an out-of-line FREE function.  It runs a few
+// thousand times per solve but, inlined at every cascade-write and flush site, it was
+// ~8 K of the K1 variant's 23 K SASS instructions and pushed the hot read/relax loop out of
+// the instruction cache (ncu: 17 % of C2 stall samples "no instruction").  A member
+// function would take `this` and force the Worker into local memory (measured +50 % in
+// round 2), so everything it needs is passed by value.  Per-slot Vyukov sequence numbers:
+// one fetch-add claims ceil(n/bs) tickets; slot waits, element stores and publications
+// proceed lane-parallel.  Returns false after raising an overflow error (spin timeout) or
+// when the solve is stopping.
+template <class E, int L2K>
+__device__ __noinline__ bool ring_write_cold(const KParams* pp, int rid, const E* base, int start, int n, int cap,
+                                             int lane) {
+  const KParams& p = *pp;
+  const int bs = p.bs;
+  const int nseg = (n + bs - 1) / bs;
+  unsigned long long t = 0;
+  unsigned long long* wpr = p.ptrs + (size_t)rid * 32;
+  if (lane == 0) t = atomicAdd(wpr, (unsigned long long)nseg);
+  t = __shfl_sync(FULL, t, 0);
+  bool ok = true;
+  for (int sg = lane; sg < nseg; sg += 32) {  // wait until the claimed slots are free
+    const unsigned long long tk = t + sg, slot = tk & p.bn_mask;
+    const unsigned long long* sp = p.seq + (size_t)rid * (p.bn_mask + 1) + slot;
+    unsigned long long t0 = 0;
+    int spins = 0, ns = 32;
+    while (ok && ld_acquire(sp) != tk) {
+      if (++spins % 64 == 0) {
+        if (ld_relaxed(p.ctl + C_STOP) != 0) { ok = false; break; }
+        const unsigned long long now = globaltimer_ns();
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > p.spin_timeout_ns) {
+          if (atomicCAS(p.ctl + C_ERR, 0ull, (unsigned long long)ERR_OVERFLOW) == 0ull) {
+            p.ctl[C_DIAG + 0] = (unsigned long long)rid;
+            p.ctl[C_DIAG + 1] = slot;
+            p.ctl[C_DIAG + 2] = ld_relaxed(wpr);
+            p.ctl[C_DIAG + 3] = ld_relaxed(wpr + 16);
+          }
+          __threadfence();
+          st_release(p.ctl + C_STOP, 1ull);
+          ok = false;
+          break;
+        }
+      }
+      __nanosleep(ns);
+      if (ns < 1024) ns <<= 1;
+    }
+  }
+  if (!__all_sync(FULL, ok)) return false;
+  for (int i = lane; i < n; i += 32) {
+    const int sg = i / bs;
+    reinterpret_cast<E*>(p.data)[((size_t)rid * (p.bn_mask + 1) + ((t + sg) & p.bn_mask)) * bs + (i - sg * bs)] =
+        base[(unsigned)(start + i) % (unsigned)cap];
+  }
+  __threadfence();
+  __syncwarp();
+  for (int sg = lane; sg < nseg; sg += 32) {
+    const unsigned long long tk = t + sg, slot = tk & p.bn_mask;
+    const size_t i = (size_t)rid * (p.bn_mask + 1) + slot;
+    p.cnt[i] = (uint32_t)min(bs, n - sg * bs);
+    st_release(p.seq + i, tk + 1);
+  }
+  __syncwarp();
+  bool bump = true;
+  if (L2K == L2K_BUCKET && p.bwin > 0) {  // managed floor: only near-window rings wake readers
+    unsigned long long e = 0;
+    if (lane == 0) e = ld_relaxed(p.ctl + C_EPOCH);
+    const int emod = (int)(__shfl_sync(FULL, e, 0) % (unsigned long long)p.bmax);
+    const int rel = rid >= emod ? rid - emod : rid + p.bmax - emod;
+    bump = rel == 0 || rel == p.bmax - 1;
+  }
+  if (bump && lane == 0) red_add(p.ctl + C_GEN, 1ull);
+  return true;
+}
+
+// Raise a queue error (QueueOverflowError analogue) and stop every warp: cold, out of line.
+static __device__ __noinline__ void raise_error_cold(unsigned long long* ctl, int code, unsigned long long a,
+                                              unsigned long long b, unsigned long long c, unsigned long long d) {
+  if (atomicCAS(ctl + C_ERR, 0ull, (unsigned long long)code) == 0ull) {
+    ctl[C_DIAG + 0] = a;
+    ctl[C_DIAG + 1] = b;
+    ctl[C_DIAG + 2] = c;
+    ctl[C_DIAG + 3] = d;
+  }
+  __threadfence();
+  st_release(ctl + C_STOP, 1ull);
+}
+
 template <int K, int L2K, int CM, int L1T>
 struct Worker {
   using Tr = DT<K>;
@@ -218,6 +310,12 @@ struct Worker {
   // Raise a queue error (QueueOverflowError analogue) and stop every warp.
   __device__ void raise_error(int code, unsigned long long a, unsigned long long b,
                               unsigned long long c, unsigned long long d) {
+#if MLMQ_COLD_RING >= 2
+    if (!kDebug) {
+      raise_error_cold(p.ctl, code, a, b, c, d);
+      return;
+    }
+#endif
     if (atomicCAS(p.ctl + C_ERR, 0ull, (unsigned long long)code) == 0ull) {
       p.ctl[C_DIAG + 0] = a;
       p.ctl[C_DIAG + 1] = b;
@@ -383,6 +481,13 @@ struct Worker {
   __device__ void ring_write(int rid, const E* base, int start, int n, int cap) {
     LOC();
     if (n <= 0) return;
+#if MLMQ_COLD_RING
+    if (!kDebug) {  // the debug builds keep the inlined form with its wait-state hooks
+      count(M_L2A, 1);
+      ring_write_cold<E, L2K>(&p, rid, base, start, n, cap, lane);
+      return;
+    }
+#endif
     const int bs = p.bs;
     const int nseg = (n + bs - 1) / bs;
     unsigned long long t = 0;

@@ -58,6 +58,13 @@ for r in srows:
                 except ValueError:
                     pass
 tot = sum(a[0] for a in acc) or 1
+# stall reasons from the raw pc-sampling counters (the source page's per-line stall
+# columns shift when CUDA and SASS rows are interleaved)
+pre = "smsp__pcsamp_warps_issue_stalled_"
+raw_st = {k[len(pre):]: float(v[0]) for k, v in M.items()
+          if k.startswith(pre) and not k.endswith("_not_issued") and v[0] not in ("", "n/a")}
+if raw_st:
+    reasons = {"stall_" + k: x for k, x in raw_st.items()}
 rt = sum(reasons.values()) or 1
 print("\n## Stall reasons (share of warp samples)\n\n| reason | % |\n|---|---|")
 for h, v in sorted(reasons.items(), key=lambda x: -x[1])[:8]:
