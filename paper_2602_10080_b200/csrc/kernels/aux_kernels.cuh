@@ -374,6 +374,27 @@ __global__ void relabel_keys_kernel(const uint32_t* indeg, unsigned long long n,
   if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
 }
 
+// Per class key: number of vertices and in-edges (mass[256] and cnt[256], zeroed by the
+// caller) -- the host picks the hot prefix that takes 95 % of the edge targets.
+__global__ void class_mass_kernel(const uint32_t* indeg, const uint8_t* key, unsigned long long n,
+                                  unsigned long long* mass, unsigned long long* cnt) {
+  __shared__ unsigned long long sm[256], sc[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sm[i] = sc[i] = 0;
+  __syncthreads();
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = tid; i < n; i += stride) {
+    atomicAdd(&sm[key[i]], (unsigned long long)indeg[i]);
+    atomicAdd(&sc[key[i]], 1ull);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (sc[i]) {
+      atomicAdd(mass + i, sm[i]);
+      atomicAdd(cnt + i, sc[i]);
+    }
+}
+
 // perm[iperm[i]] = i; ndeg[i] = degree of the vertex that becomes row i.
 __global__ void relabel_perm_kernel(const uint32_t* iperm, const unsigned long long* off, unsigned long long n,
                                     uint32_t* perm, unsigned long long* ndeg) {

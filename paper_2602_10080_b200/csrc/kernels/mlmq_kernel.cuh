@@ -21,7 +21,7 @@
 namespace mlmq {
 
 #ifndef MLMQ_COLD_RING
-#define MLMQ_COLD_RING 1
+#define MLMQ_COLD_RING 0  // measured slower (caller-side spills in the hot loop), see r2_experiments.md
 #endif
 
 // The L2 block-ring writer (l2.py:96-114) as an out-of-line FREE function.  It runs a few

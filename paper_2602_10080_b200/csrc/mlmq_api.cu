@@ -209,6 +209,7 @@ struct mlmq_graph {
   uint32_t* d_perm = nullptr;
   std::vector<uint32_t> h_perm;
   int relabel_state = 0;
+  unsigned long long hot_n = 0;  // relabeled: the prefix of vertices that takes 95 % of the edge targets
   void* d_gather = nullptr;  // caller-order copy of the distances (n x 8 bytes)
   uint32_t* h_stage = nullptr;           // pinned staging of u32 results (copy_dist_u64)
   unsigned long long stage_cap = 0;
@@ -378,6 +379,23 @@ int ensure_relabel(mlmq_graph* g) {
     relabel_keys_kernel<<<blocks, 256, 0, g->stream>>>(indeg, n, key, val, (unsigned int*)g->d_scratch);
     RL(cudaGetLastError(), "launch");
     RL(cudaMemcpyAsync(&mx, g->d_scratch, 4, cudaMemcpyDeviceToHost, g->stream), "copy");
+    {  // the hot prefix: classes in key order until 95 % of the in-edges are covered
+      unsigned long long* cm = nullptr;
+      RL(cudaMalloc(&cm, 512 * 8), "alloc");
+      cudaMemsetAsync(cm, 0, 512 * 8, g->stream);
+      class_mass_kernel<<<blocks, 256, 0, g->stream>>>(indeg, key, n, cm, cm + 256);
+      std::vector<unsigned long long> hm(512);
+      cudaError_t e = cudaMemcpyAsync(hm.data(), cm, 512 * 8, cudaMemcpyDeviceToHost, g->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+      cudaFree(cm);
+      RL(e, "class mass");
+      unsigned long long acc = 0, cnt = 0;
+      for (int k = 0; k < 256 && (double)acc < 0.95 * (double)m; ++k) {
+        acc += hm[k];
+        cnt += hm[256 + k];
+      }
+      g->hot_n = cnt;
+    }
     RL(cudaStreamSynchronize(g->stream), "in-degrees");
     cudaFree(indeg);
     indeg = nullptr;
@@ -629,7 +647,8 @@ void apply_l2_window(mlmq_graph* g, int dk) {
   cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g->device);
   cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
   cudaGetLastError();
-  const size_t bytes = (size_t)g->n * (dk == DK_U64 ? 8 : 4);
+  // a relabeled graph: only its hot prefix (95 % of the edge targets) needs to persist
+  const size_t bytes = (size_t)(g->relabel_state == 1 && g->hot_n ? g->hot_n : g->n) * (dk == DK_U64 ? 8 : 4);
   if (maxp <= 0 || maxw <= 0 || (frac < 0.f && (bytes > (size_t)maxp || bytes > (size_t)maxw))) {
     if (g->l2win_set) {  // a different distance kind no longer fits: drop the window
       cudaStreamAttrValue a = {};
