@@ -337,15 +337,16 @@ int ensure_partition(mlmq_graph* g, uint32_t h) {
 // the vertex ids by key, the new row offsets (scan) and the rows copied with their targets
 // renamed.  Sources map through perm, results gather back to caller order, so the ABI is
 // unchanged.  Auto policy: only when the graph is skewed (max in-degree >= 32 x mean) and
-// its distance words outgrow half of L2 (n x 4 B > 64 MB: C4 20.3 -> 19.0 ms, C5 6.58 ->
-// 6.51 ms; C2, whose 16.8 MB of distances stay L2-resident anyway, measured 1.40 -> 1.57
-// ms relabeled, so it keeps the caller order); MLMQ_RELABEL=0/1 forces it off/on.
+// its distance words fill half of L2 (n x 4 B >= 64 MiB: C4 20.3 -> 19.0 ms, 18.1 ms with
+// the hot-prefix L2 window; C5 6.58 -> 6.51 ms; C2, whose 16.8 MB of distances stay
+// L2-resident anyway, measured 1.40 -> 1.57 ms relabeled, so it keeps the caller order);
+// MLMQ_RELABEL=0/1 forces it off/on.
 int ensure_relabel(mlmq_graph* g) {
   if (g->relabel_state) return MLMQ_OK;
   const char* env = getenv("MLMQ_RELABEL");
   const int force = env ? atoi(env) : -1;
   if (force == 0 || g->nparts > 1 || g->n < 2 || g->m == 0 || g->n >= 0xFFFFFFFFull ||
-      (force < 0 && g->n * 4ull <= (64ull << 20))) {
+      (force < 0 && g->n * 4ull < (64ull << 20))) {
     g->relabel_state = 2;
     return MLMQ_OK;
   }
@@ -647,8 +648,12 @@ void apply_l2_window(mlmq_graph* g, int dk) {
   cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g->device);
   cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
   cudaGetLastError();
-  // a relabeled graph: only its hot prefix (95 % of the edge targets) needs to persist
-  const size_t bytes = (size_t)(g->relabel_state == 1 && g->hot_n ? g->hot_n : g->n) * (dk == DK_U64 ? 8 : 4);
+  // A relabeled graph whose distances outgrow the carve-out persists only its hot prefix
+  // (95 % of the edge targets): C4 19.05 -> 18.12 ms.  A whole array that fits keeps the
+  // whole-array window (C5 relabeled: hot prefix only 6.62 ms vs 6.51).
+  const size_t esz = dk == DK_U64 ? 8 : 4;
+  size_t bytes = (size_t)g->n * esz;
+  if (g->relabel_state == 1 && g->hot_n && maxp > 0 && bytes > (size_t)maxp) bytes = (size_t)g->hot_n * esz;
   if (maxp <= 0 || maxw <= 0 || (frac < 0.f && (bytes > (size_t)maxp || bytes > (size_t)maxw))) {
     if (g->l2win_set) {  // a different distance kind no longer fits: drop the window
       cudaStreamAttrValue a = {};
