@@ -19,6 +19,13 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 #define MLMQ_MINB 2
 #endif
 constexpr int kWarpsPerBlockMax = MLMQ_WPB;
+#ifndef MLMQ_F32_WPB
+#define MLMQ_F32_WPB MLMQ_WPB
+#endif
+// The f32-distance kernels are compiled with MLMQ_WPB = MLMQ_F32_WPB (Makefile): C5 measured
+// 6.59 -> 6.20 ms with 10-warp CTAs (20 warps/SM), while the u32 kernels lose with them
+// (C2 1.39 -> 1.80 ms, C4 19.1 -> 31.5 ms), so only dk = f32 uses it.
+constexpr int kF32WarpsPerBlock = MLMQ_F32_WPB;
 
 // MLMQ_ASYNC=1: the flattened expansion stages the next step's adjacency into shared
 // memory with cp.async (LDGSTS) while the current step runs, so two steps of DRAM loads

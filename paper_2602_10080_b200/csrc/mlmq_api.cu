@@ -499,7 +499,7 @@ int launch_shape(mlmq_graph* g, const mlmq_config_t* c, int dk, LaunchShape* s) 
     return MLMQ_EINVAL;
   }
   s->smem_per_warp = (int)bytes;
-  s->wpb = (int)std::min<long long>(kWarpsPerBlockMax, dyn_max / bytes);
+  s->wpb = (int)std::min<long long>(dk == DK_F32 ? kF32WarpsPerBlock : kWarpsPerBlockMax, dyn_max / bytes);
   static std::mutex attr_mu;
   static std::unordered_set<const void*> attr_done;
   {
@@ -1959,7 +1959,7 @@ int mlmq_queue_stress(mlmq_queue* q, int32_t writers, int32_t readers, uint64_t 
   p.G = writers + readers;
   if (cudaMemsetAsync(q->d_n, 0, 8, g->stream) != cudaSuccess) { cleanup(); CK(cudaGetLastError()); }
   CK(cudaEventRecord(g->ev0, g->stream));
-  const int wpb = std::max(1, q->sh.wpb);
+  const int wpb = std::max(1, std::min(q->sh.wpb, 9));  // queue_harness_kernel: __launch_bounds__(288)
   if (harness_launch(q->l2k, p, h, writers + readers, wpb, (size_t)q->sh.smem_per_warp, g->stream) != 0) {
     cleanup();
     set_last_error("queue stress launch failed: %s", cudaGetErrorString(cudaGetLastError()));
