@@ -211,6 +211,10 @@ struct mlmq_graph {
   int relabel_state = 0;
   unsigned long long hot_n = 0;  // relabeled: the prefix of vertices that takes 95 % of the edge targets
   void* d_gather = nullptr;  // caller-order copy of the distances (n x 8 bytes)
+  // per-vertex arrays packed into one buffer [off | nlight | dist] so one persisting L2
+  // window covers every random per-vertex load of K1 (pack_vertex_arrays)
+  void* d_vtx = nullptr;
+  size_t vtx_bytes = 0;
   uint32_t* h_stage = nullptr;           // pinned staging of u32 results (copy_dist_u64)
   unsigned long long stage_cap = 0;
   cudaEvent_t chunk_ev[8] = {};
@@ -638,6 +642,37 @@ bool debug_enabled() {
 // Default: only when the whole array fits the persisting carve-out (B200: 79 MB; C5's
 // 67 MB: 6.85 -> 6.65 ms, C2 neutral; a partial window on C4's 268 MB costs 16 %).
 // MLMQ_L2PERSIST=<fraction> forces a window of that fraction, 0 turns it off.
+// Pack off, nlight and dist into one buffer (after the relabel and the light/heavy
+// partition, which replace off/nlight) so a single persisting window can hold all three
+// when they fit the carve-out together (C2: 33.5 + 16.8 + 16.8 MB).  MLMQ_VTXPACK=1.
+void pack_vertex_arrays(mlmq_graph* g) {
+  static const int on = [] {
+    const char* e = getenv("MLMQ_VTXPACK");
+    return e ? atoi(e) : 0;
+  }();
+  if (!on || g->d_vtx || !g->d_nlight || g->nparts > 1) return;
+  const size_t ob = (g->n + 1) * 8, nb = g->n * 4, db = std::max<size_t>(8, g->n * 8);
+  const size_t nb_al = (nb + 255) / 256 * 256, ob_al = (ob + 255) / 256 * 256;
+  unsigned char* buf = nullptr;
+  if (cudaMalloc(&buf, ob_al + nb_al + db) != cudaSuccess) { cudaGetLastError(); return; }
+  if (cudaMemcpyAsync(buf, g->d_off, ob, cudaMemcpyDeviceToDevice, g->stream) != cudaSuccess ||
+      cudaMemcpyAsync(buf + ob_al, g->d_nlight, nb, cudaMemcpyDeviceToDevice, g->stream) != cudaSuccess ||
+      cudaStreamSynchronize(g->stream) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(buf);
+    return;
+  }
+  cudaFree(g->d_off);
+  cudaFree(g->d_nlight);
+  cudaFree(g->d_dist);
+  g->d_off = (unsigned long long*)buf;
+  g->d_nlight = (uint32_t*)(buf + ob_al);
+  g->d_dist = buf + ob_al + nb_al;
+  g->d_vtx = buf;
+  g->vtx_bytes = ob_al + nb_al;  // + the distance words in use
+  g->l2win_set = false;
+}
+
 void apply_l2_window(mlmq_graph* g, int dk) {
   static const float frac = [] {
     const char* e = getenv("MLMQ_L2PERSIST");
@@ -654,6 +689,11 @@ void apply_l2_window(mlmq_graph* g, int dk) {
   const size_t esz = dk == DK_U64 ? 8 : 4;
   size_t bytes = (size_t)g->n * esz;
   if (g->relabel_state == 1 && g->hot_n && maxp > 0 && bytes > (size_t)maxp) bytes = (size_t)g->hot_n * esz;
+  void* base = g->d_dist;
+  if (g->d_vtx && maxp > 0 && g->vtx_bytes + (size_t)g->n * esz <= (size_t)maxp) {  // packed [off|nlight|dist]
+    base = g->d_vtx;
+    bytes = g->vtx_bytes + (size_t)g->n * esz;
+  }
   if (maxp <= 0 || maxw <= 0 || (frac < 0.f && (bytes > (size_t)maxp || bytes > (size_t)maxw))) {
     if (g->l2win_set) {  // a different distance kind no longer fits: drop the window
       cudaStreamAttrValue a = {};
@@ -670,7 +710,7 @@ void apply_l2_window(mlmq_graph* g, int dk) {
   if (cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize) != cudaSuccess || cur < lim)
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
   cudaStreamAttrValue a = {};
-  a.accessPolicyWindow.base_ptr = g->d_dist;
+  a.accessPolicyWindow.base_ptr = base;
   a.accessPolicyWindow.num_bytes = win;
   a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)lim / (double)win);
   a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -910,6 +950,7 @@ int run_once(mlmq_graph* g, unsigned long long source, const mlmq_config_t* c, i
   if (!io && (st = ensure_relabel(g))) return st;
   if (g->relabel_state == 1) source = g->h_perm[source];
   if (sh.hvy_cap && (st = ensure_partition(g, heavy_bits(g, c)))) return st;
+  if (sh.hvy_cap) pack_vertex_arrays(g);
   if ((st = ensure_workspace(g, c, sh, hub_chunk, G))) return st;
   if (g->metrics_cap < (unsigned long long)G) {
     cudaFree(g->d_metrics);
@@ -1486,6 +1527,12 @@ void mlmq_graph_destroy(mlmq_graph* g) {
   }
   if (g->stream) cudaStreamSynchronize(g->stream);
   ws_free(g->ws);
+  if (g->d_vtx) {  // off / nlight / dist live inside the packed buffer
+    cudaFree(g->d_vtx);
+    g->d_off = nullptr;
+    g->d_nlight = nullptr;
+    g->d_dist = nullptr;
+  }
   cudaFree(g->d_off);
   cudaFree(g->d_adj);
   cudaFree(g->d_dist);
