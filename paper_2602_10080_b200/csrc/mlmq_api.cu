@@ -290,10 +290,10 @@ struct LaunchShape {
   int bscratch = 0;
 };
 
-// The light/heavy split applies to the FIFO L2 of an unpartitioned graph; returns the
+// The light/heavy split applies to the FIFO L2 (whole graphs and shards); returns the
 // threshold as weight bits (0 = off).
 uint32_t heavy_bits(const mlmq_graph* g, const mlmq_config_t* c) {
-  if (c->l2_type != MLMQ_L2_FIFO || g->nparts > 1 || c->unit_weights || g->wkind == MLMQ_W_UNIT) return 0;
+  if (c->l2_type != MLMQ_L2_FIFO || c->unit_weights || g->wkind == MLMQ_W_UNIT) return 0;
   if (g->wkind == MLMQ_W_F32) {
     if (!(c->heavy_delta_f > 0.f)) return 0;
     uint32_t b;

@@ -136,6 +136,21 @@ def test_c4_sharded_matches_golden_hash(c4_graph, parts):
     assert oracle.dist_sha256(res.local_dist) == BIG["c4"]["dist_sha256"], parts
 
 
+def test_sharded_light_heavy_split_matches():
+    # shards with the light/heavy split (heavy tokens drained inside each superstep)
+    from paper_2602_10080_b200.sharded import sssp_solve_sharded
+    g = generate_graph("rmat", seed=4, scale=12, edge_factor=16, wmin=1, wmax=255)
+    want = oracle.dijkstra_u64(g.row_offsets, g.col_indices, g.weights, 0)
+    for P in (2, 4, 8):
+        res = sssp_solve_sharded(g, 0, P, MlmqConfig(l2_type="fifo"), EngineConfig(heavy_delta=24))
+        assert np.array_equal(res.local_dist, want), P
+    from bench import build_graph
+    c2 = build_graph("c2")
+    for P in (2, 8):
+        res = sssp_solve_sharded(c2, 0, P, MlmqConfig(l2_type="fifo"), EngineConfig(heavy_delta=24))
+        assert oracle.dist_sha256(res.local_dist) == C2_DIST, P
+
+
 def test_c2_sharded_matches_reference_hash():
     from bench import build_graph
     from paper_2602_10080_b200.sharded import sssp_solve_sharded
